@@ -1,0 +1,63 @@
+// Microbenchmark: per-SM throughput of the instruction classes the KV codec
+// kernels lean on (fp64 add/mul, f64<->f32 converts, shuffles, int div).
+#include <cstdio>
+#include <cuda_runtime.h>
+#define N_ITER 4096
+template <int OP>
+__global__ void k(float* out, double* dout, int seed) {
+  double a = threadIdx.x * 1.0000001 + seed, b = 1.0 + 1e-9 * seed, c = a * 0.5, d = a * 0.25;
+  float fa = threadIdx.x * 1.01f, fb = fa * 0.5f, fc = fa * 0.25f, fd = fa * 0.125f;
+  unsigned ua = threadIdx.x + 12345u, ub = ua * 7u + 1, uc = ua ^ 0x55u, ud = ua + 99u;
+  unsigned dv = (seed & 0xFFFF) + 37;
+#pragma unroll 16
+  for (int i = 0; i < N_ITER; ++i) {
+    if (OP == 0) { a = a + b; c = c + b; d = d + b; fa = fa + 1.0f; }                  // DADD x3 indep
+    if (OP == 1) { a = a * b; c = c * b; d = d * b; }                                   // DMUL
+    if (OP == 2) { fa = __double2float_rn(a + fa); fb = __double2float_rn(c + fb); }   // F2F.F32.F64 (+DADD)
+    if (OP == 3) { a += (double)fa; c += (double)fb; fa += 1.0f; fb += 1.0f; }          // F2F.F64.F32
+    if (OP == 4) { fa += __shfl_xor_sync(0xffffffff, fb, 1); fb += __shfl_xor_sync(0xffffffff, fc, 2); fc += __shfl_xor_sync(0xffffffff, fd, 4); fd += __shfl_xor_sync(0xffffffff, fa, 8);}  // SHFL
+    if (OP == 5) { ua = ua / dv + i; ub = ub / dv + i; uc = uc / dv + i; ud = ud / dv + i; }  // u32 div
+    if (OP == 6) { fa = fa + fb; fb = fb + fc; fc = fc + fd; fd = fd + fa; }           // FADD (dep)
+    if (OP == 7) { fa = __fmaf_rn(fa, 1.0001f, fb); fb = __fmaf_rn(fb, 1.0001f, fc); fc = __fmaf_rn(fc, 1.0001f, fd); fd = __fmaf_rn(fd, 1.0001f, fa); }
+    if (OP == 8) { fa = rintf(fa * 1.3f); fb = rintf(fb * 1.3f); fc = rintf(fc*1.3f); fd = rintf(fd*1.3f);}  // FRND
+    if (OP == 9) { fa += __uint2float_rn(ua + i); fb += __uint2float_rn(ub + i); fc += __uint2float_rn(uc+i); fd += __uint2float_rn(ud+i);} // I2F
+    if (OP == 10) { ua = ua * 0x9E3779B9u + (ua >> 7); ub = ub * 0x9E3779B9u + (ub >> 7); uc = uc*0x9E3779B9u + (uc>>7); ud = ud*0x9E3779B9u+(ud>>7);} // IMAD+SHF
+    if (OP == 11) { fa = __frcp_rn(fa + 1.0f); fb = __frcp_rn(fb + 1.0f);}                  // frcp_rn
+    if (OP == 12) { a = __ddiv_rn(a, b + i); c = __ddiv_rn(c, b + i); }                     // DDIV
+    if (OP == 13) { fa = __fdiv_rn(fa, fb + 1.0f); fb = __fdiv_rn(fb, fc + 2.0f); }         // FDIV
+  }
+  if (a + c + d + fa + fb + fc + fd + ua + ub + uc + ud == 0.123) { out[0] = fa; dout[0] = a; }
+}
+template <int OP> float run(const char* name, int per_iter_ops, float* o, double* d) {
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int blocks = 148 * 8, threads = 256;
+  k<OP><<<blocks, threads>>>(o, d, 1);
+  cudaEventRecord(e0);
+  k<OP><<<blocks, threads>>>(o, d, 2);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double ops = double(blocks) * threads * N_ITER * per_iter_ops;
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("%-28s %8.3f ms  %9.1f Gop/s  %6.1f op/clk/SM (at %d MHz max)\n", name, ms, ops / ms / 1e6,
+         ops / (ms * 1e-3) / 148 / (clk * 1e3), clk / 1000);
+  return ms;
+}
+int main() {
+  float* o; double* d; cudaMalloc(&o, 64); cudaMalloc(&d, 64);
+  run<0>("DADD x3 (+FADD)", 3, o, d);
+  run<1>("DMUL x3", 3, o, d);
+  run<2>("F2F.F32.F64 x2 (+DADD x2)", 2, o, d);
+  run<3>("F2F.F64.F32 x2 (+DADD x2)", 2, o, d);
+  run<4>("SHFL x4 (+FADD)", 4, o, d);
+  run<5>("u32 div x4", 4, o, d);
+  run<6>("FADD x4 dep-chain", 4, o, d);
+  run<7>("FFMA x4 dep-chain", 4, o, d);
+  run<8>("FRND x4 (+FMUL)", 4, o, d);
+  run<9>("I2F x4 (+FADD)", 4, o, d);
+  run<10>("IMAD+SHF x4", 4, o, d);
+  run<11>("frcp_rn x2", 2, o, d);
+  run<12>("ddiv_rn x2", 2, o, d);
+  run<13>("fdiv_rn x2", 2, o, d);
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
