@@ -1,0 +1,121 @@
+/*
+ * kvc.h — C ABI of the B200 KV-cache compression codec (libkvc.so).
+ *
+ * Drop-in boundary for the reference's codec hot path
+ * (/root/reference/pkg/src/kvpilot/pipeline/).  The reference is pure
+ * Python, so "its FFI" is the pipeline's public call surface; each entry
+ * point below names the reference function it replaces:
+ *
+ *   kvc_plan_create     <- parse_strategy_id + config validation
+ *                          (strategy.py:68-109, quantize.py:26-62,
+ *                           transforms.py:25-30, codecs.py:32-38)
+ *   kvc_encode          <- the encode closure of compress():
+ *                          apply_transform -> classify_heads -> quantize ->
+ *                          encode_lossless (compress.py:122-125)
+ *   kvc_decode          <- decompress()'s decode closure: decode_lossless ->
+ *                          dequantize -> invert_transform (compress.py:150-151)
+ *   kvc_decode_paged    <- same, writing into a paged KV cache (extension)
+ *   kvc_read_status     <- the ValueError / CodecError raises of
+ *                          tensors.py:41-42 and codecs.py:94,166,171,288,389,413,430
+ *   kvc_last_error      <- exception message text
+ *
+ * Conventions: plain pointers and sizes only.  `kv`, `payload`, `metadata`,
+ * `block_offsets`, `out` and `workspace` are DEVICE pointers owned by the
+ * caller and sized with the query functions; `head_classes` is a HOST array.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  No call
+ * allocates device memory; all device work is stream-ordered, and plans are
+ * immutable after creation (safe to share across threads and streams).
+ * Every function returns a kvc_status; on failure kvc_last_error() holds a
+ * thread-local message.
+ */
+#ifndef KVC_H_
+#define KVC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kvc_plan kvc_plan;
+
+typedef enum {
+  KVC_OK = 0,
+  KVC_ERR_CONFIG = 1, /* ValueError: bad strategy id / shape / options      */
+  KVC_ERR_CODEC = 2,  /* CodecError: malformed or mismatched payload          */
+  KVC_ERR_CUDA = 3,   /* CUDA runtime failure                                 */
+  KVC_ERR_VALUE = 4   /* ValueError raised by the data (non-finite values)    */
+} kvc_status;
+
+enum { KVC_DTYPE_BF16 = 0, KVC_DTYPE_F32 = 1 };
+
+/* device status word flags (kvc_read_status) */
+enum {
+  KVC_FLAG_NONFINITE_INPUT = 1u,     /* tensors.py:41-42 on the input          */
+  KVC_FLAG_NONFINITE_TRANSFORM = 2u, /* transform overflowed float32           */
+  KVC_FLAG_CODEC = 4u,               /* truncated / trailing / length mismatch */
+  KVC_FLAG_CAPACITY = 8u,            /* entropy block exceeded its scratch slot */
+  KVC_FLAG_FP16_RANGE = 16u          /* a zero/scale overflowed float16 (the
+                                        reference reproduces this; decode then
+                                        yields +-inf and raises ValueError)    */
+};
+
+typedef struct {
+  int64_t block_symbols; /* codec block (entropy / rle framing); multiple of 8; 0 -> 4096 */
+  int32_t in_dtype;      /* KVC_DTYPE_BF16 (serving cache) or KVC_DTYPE_F32 (reference) */
+  int32_t out_dtype;     /* decode output dtype                                 */
+  int32_t reserved[8];
+} kvc_options;
+
+/* Create a plan for one KV tensor shape (layers, heads, tokens, channels)
+ * and one strategy id, e.g. "t=hadamard;q=uniform,b=4,g=32;c=none".
+ * Accepts the reference grammar (strategy.py:8-19) plus the extension kinds
+ * t=affine, q=uchan / mixlayer / mixtok. */
+int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t layers, int64_t heads, int64_t tokens,
+                    int64_t channels, const kvc_options* options);
+int kvc_plan_destroy(kvc_plan* plan);
+
+/* Canonical strategy id of the plan (NUL-terminated, owned by the plan). */
+const char* kvc_plan_strategy_id(const kvc_plan* plan);
+
+int64_t kvc_metadata_bytes(const kvc_plan* plan);  /* exact metadata size          */
+int64_t kvc_payload_capacity(const kvc_plan* plan); /* upper bound on payload size   */
+int64_t kvc_workspace_bytes(const kvc_plan* plan);  /* scratch needed by encode/decode */
+int64_t kvc_max_blocks(const kvc_plan* plan);       /* block_offsets needs max_blocks+1 */
+
+/* Payload bytes when they do not depend on the data (codec none), else -1:
+ * then the size is block_offsets[nblocks] on the device after kvc_encode. */
+int64_t kvc_static_payload_bytes(const kvc_plan* plan, const uint8_t* head_classes);
+/* Number of codec blocks for these head classes (0 for codec none). */
+int64_t kvc_num_blocks(const kvc_plan* plan, const uint8_t* head_classes);
+
+/* Encode one KV tensor.  `kv` is (L,H,T,C) row-major in the plan's in_dtype.
+ * `head_classes` (host, L*H bytes, nonzero = retrieval head) is required for
+ * q=mixed / mixlayer and ignored otherwise.  Writes metadata (exactly
+ * kvc_metadata_bytes), payload, and for rle/entropy the block offset table
+ * (uint64, nblocks+1 entries, offsets into payload). */
+int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
+               uint64_t* block_offsets, void* workspace, void* stream);
+
+/* Decode into a contiguous (L,H,T,C) tensor of the plan's out_dtype. */
+int kvc_decode(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
+               const uint64_t* block_offsets, void* out, void* workspace, void* stream);
+
+/* Decode into a paged cache: element (l,h,t,c) lands at
+ *   base + l*layer_stride + (block_table[t / page_tokens]*page_tokens + t % page_tokens)*H*C + h*C + c
+ * (vLLM layout [num_pages, page_tokens, heads, channels] per layer; strides in elements). */
+int kvc_decode_paged(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
+                     const uint64_t* block_offsets, void* page_base, const int32_t* block_table, int64_t page_tokens,
+                     int64_t layer_stride, void* workspace, void* stream);
+
+/* Synchronise `stream` and read (then clear) the device status word. */
+int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_t* flags);
+
+const char* kvc_last_error(void);
+const char* kvc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVC_H_ */

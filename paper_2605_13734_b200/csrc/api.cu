@@ -1,0 +1,458 @@
+// C ABI (include/kvc.h): plan creation, size queries, encode / decode.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "kvc_internal.h"
+
+using namespace kvc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(KVC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- id parser
+// Grammar of strategy.py:8-19 (and the same validations: quantize.py:26-62,
+// transforms.py:25-30, codecs.py:32-38) plus the extension kinds.
+bool parse_int(const std::string& s, int& out) {
+  if (s.empty()) return false;
+  size_t i = (s[0] == '-' || s[0] == '+') ? 1 : 0;
+  if (i == s.size()) return false;
+  for (size_t k = i; k < s.size(); ++k)
+    if (s[k] < '0' || s[k] > '9') return false;
+  long v = strtol(s.c_str(), nullptr, 10);
+  if (v < -1000000 || v > 1000000) return false;
+  out = (int)v;
+  return true;
+}
+
+bool parse_double(const std::string& s, double& out) {
+  if (s.empty()) return false;
+  char* end = nullptr;
+  out = strtod(s.c_str(), &end);
+  return end && *end == '\0';
+}
+
+std::string py_float_repr(double v) {
+  char buf[64];
+  for (int p = 1; p <= 17; ++p) {
+    snprintf(buf, sizeof buf, "%.*g", p, v);
+    if (strtod(buf, nullptr) == v) break;
+  }
+  std::string s(buf);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";  // Python repr keeps a '.0'
+  return s;
+}
+
+std::string trim(const std::string& s) {
+  size_t a = s.find_first_not_of(" \t\r\n\f\v"), b = s.find_last_not_of(" \t\r\n\f\v");
+  return a == std::string::npos ? std::string() : s.substr(a, b - a + 1);
+}
+
+std::vector<std::string> split(const std::string& s, char c) {
+  std::vector<std::string> out;
+  size_t start = 0;
+  for (;;) {
+    size_t p = s.find(c, start);
+    out.push_back(s.substr(start, p == std::string::npos ? std::string::npos : p - start));
+    if (p == std::string::npos) break;
+    start = p + 1;
+  }
+  return out;
+}
+
+int parse_strategy(const char* text, Geo& g, double& rho, std::string& canon) {
+  if (!text) return fail(KVC_ERR_CONFIG, "strategy id is NULL");
+  std::string s = trim(text);
+  auto seg = split(s, ';');
+  if (seg.size() != 3)
+    return fail(KVC_ERR_CONFIG, "strategy id must have 3 ';'-separated segments, got " + std::to_string(seg.size()));
+  auto kv = [](const std::string& tok, std::string& k, std::string& v) {
+    size_t p = tok.find('=');
+    if (p == std::string::npos) return false;
+    k = tok.substr(0, p);
+    v = tok.substr(p + 1);
+    return true;
+  };
+  std::string k, v;
+  if (!kv(seg[0], k, v) || k != "t") return fail(KVC_ERR_CONFIG, "bad transform segment '" + seg[0] + "'");
+  if (v == "identity") g.transform = T_IDENTITY;
+  else if (v == "delta") g.transform = T_DELTA;
+  else if (v == "hadamard") g.transform = T_HADAMARD;
+  else if (v == "affine") g.transform = T_AFFINE;
+  else return fail(KVC_ERR_CONFIG, "bad transform segment '" + seg[0] + "'");
+  const std::string tname = v;
+
+  if (!kv(seg[1], k, v) || k != "q") return fail(KVC_ERR_CONFIG, "bad quant segment '" + seg[1] + "'");
+  auto qt = split(v, ',');
+  std::string kind = qt[0];
+  std::vector<std::pair<std::string, std::string>> params;
+  for (size_t i = 1; i < qt.size(); ++i) {
+    std::string a, b;
+    if (!kv(qt[i], a, b)) return fail(KVC_ERR_CONFIG, "malformed token '" + qt[i] + "' in strategy id segment '" + seg[1] + "'");
+    params.push_back({a, b});
+  }
+  auto keys_are = [&](std::initializer_list<const char*> want) {
+    if (params.size() != want.size()) return false;
+    for (const char* w : want) {
+      int n = 0;
+      for (auto& p : params) n += (p.first == w);
+      if (n != 1) return false;
+    }
+    return true;
+  };
+  auto get = [&](const char* key) {
+    for (auto& p : params)
+      if (p.first == key) return p.second;
+    return std::string();
+  };
+  std::string qcanon;
+  g.bits = 4; g.hi = 8; g.lo = 2; rho = 0.25;
+  if (kind == "uniform" || kind == "uchan") {
+    if (!keys_are({"b", "g"}))
+      return fail(KVC_ERR_CONFIG, kind + " quant needs exactly b and g in '" + seg[1] + "'");
+    int b, gs;
+    if (!parse_int(get("b"), b) || !parse_int(get("g"), gs)) return fail(KVC_ERR_CONFIG, "bad integer in '" + seg[1] + "'");
+    if (gs < 1) return fail(KVC_ERR_CONFIG, "group_size must be >= 1, got " + std::to_string(gs));
+    if (b < 1 || b > 8) return fail(KVC_ERR_CONFIG, "bits must be in 1..8, got " + std::to_string(b));
+    g.quant = kind == "uniform" ? Q_UNIFORM : Q_UCHAN;
+    g.bits = b; g.group = gs;
+    qcanon = kind + ",b=" + std::to_string(b) + ",g=" + std::to_string(gs);
+  } else if (kind == "mixed" || kind == "mixlayer" || kind == "mixtok") {
+    if (!keys_are({"hi", "lo", "g", "rho"}))
+      return fail(KVC_ERR_CONFIG, kind + " quant needs exactly hi, lo, g, rho in '" + seg[1] + "'");
+    int hi, lo, gs;
+    if (!parse_int(get("hi"), hi) || !parse_int(get("lo"), lo) || !parse_int(get("g"), gs) || !parse_double(get("rho"), rho))
+      return fail(KVC_ERR_CONFIG, "bad number in '" + seg[1] + "'");
+    if (gs < 1) return fail(KVC_ERR_CONFIG, "group_size must be >= 1, got " + std::to_string(gs));
+    if (hi < 1 || hi > 8) return fail(KVC_ERR_CONFIG, "high_bits must be in 1..8, got " + std::to_string(hi));
+    if (lo < 1 || lo > 8) return fail(KVC_ERR_CONFIG, "low_bits must be in 1..8, got " + std::to_string(lo));
+    if (hi <= lo) return fail(KVC_ERR_CONFIG, "high_bits must exceed low_bits");
+    if (!(rho >= 0.0 && rho <= 1.0)) return fail(KVC_ERR_CONFIG, "retrieval_fraction must be in [0, 1]");
+    g.quant = kind == "mixed" ? Q_MIXED : (kind == "mixlayer" ? Q_MIXLAYER : Q_MIXTOK);
+    g.hi = hi; g.lo = lo; g.group = gs;
+    qcanon = kind + ",hi=" + std::to_string(hi) + ",lo=" + std::to_string(lo) + ",g=" + std::to_string(gs) +
+             ",rho=" + py_float_repr(rho);
+  } else {
+    return fail(KVC_ERR_CONFIG, "unknown quant kind '" + kind + "' in '" + seg[1] + "'");
+  }
+  if (!kv(seg[2], k, v) || k != "c") return fail(KVC_ERR_CONFIG, "bad codec segment '" + seg[2] + "'");
+  if (v == "none") g.codec = C_NONE;
+  else if (v == "rle") g.codec = C_RLE;
+  else if (v == "entropy") g.codec = C_ENTROPY;
+  else return fail(KVC_ERR_CONFIG, "bad codec segment '" + seg[2] + "'");
+  canon = "t=" + tname + ";q=" + qcanon + ";c=" + v;
+  return KVC_OK;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Host mirror of k_setup's stream table for a given class map.
+void host_streams(const Geo& g, const uint8_t* head_classes, int n_out[1], int w[2], int64_t cnt[2]) {
+  int n = 0;
+  if (g.quant == Q_UNIFORM || g.quant == Q_UCHAN) {
+    w[0] = g.bits; cnt[0] = g.E; n = 1;
+  } else {
+    int64_t hi_cnt;
+    if (g.quant == Q_MIXTOK) {
+      hi_cnt = g.LH * g.k_tok * g.C;
+    } else {
+      int64_t nhi = 0;
+      for (int64_t i = 0; i < g.LH; ++i) nhi += head_classes && head_classes[i] ? 1 : 0;
+      hi_cnt = nhi * g.T * g.C;
+    }
+    int64_t lo_cnt = g.E - hi_cnt;
+    if (hi_cnt > 0) { w[n] = g.hi; cnt[n] = hi_cnt; ++n; }
+    if (lo_cnt > 0) { w[n] = g.lo; cnt[n] = lo_cnt; ++n; }
+  }
+  n_out[0] = n;
+}
+
+}  // namespace
+
+struct kvc_plan {
+  Plan p;
+};
+
+extern "C" {
+
+const char* kvc_last_error(void) { return g_err.c_str(); }
+const char* kvc_version(void) { return "kvc 0.1 sm_100a"; }
+
+int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t H, int64_t T, int64_t C,
+                    const kvc_options* opt) {
+  if (!out) return fail(KVC_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  Plan p;
+  memset(&p, 0, sizeof p);
+  Geo& g = p.g;
+  double rho = 0.25;
+  std::string canon;
+  int rc = parse_strategy(strategy_id, g, rho, canon);
+  if (rc) return rc;
+  if (L < 1 || H < 1 || T < 1 || C < 1)
+    return fail(KVC_ERR_CONFIG, "all dims must be >= 1");
+  g.L = L; g.H = H; g.T = T; g.C = C;
+  g.LH = L * H;
+  g.E = g.LH * T * C;
+  g.in_dtype = opt ? opt->in_dtype : KVC_DTYPE_BF16;
+  g.out_dtype = opt ? opt->out_dtype : KVC_DTYPE_BF16;
+  if ((g.in_dtype != KVC_DTYPE_BF16 && g.in_dtype != KVC_DTYPE_F32) ||
+      (g.out_dtype != KVC_DTYPE_BF16 && g.out_dtype != KVC_DTYPE_F32))
+    return fail(KVC_ERR_CONFIG, "dtype must be KVC_DTYPE_BF16 or KVC_DTYPE_F32");
+  g.block = (opt && opt->block_symbols) ? opt->block_symbols : 4096;
+  if (g.block <= 0 || g.block % 8) return fail(KVC_ERR_CONFIG, "block_symbols must be a positive multiple of 8");
+  g.uchan = g.quant == Q_UCHAN;
+  g.rowlen = g.uchan ? T : C;
+  if (g.rowlen % g.group)
+    return fail(KVC_ERR_CONFIG, "group_size " + std::to_string(g.group) + " does not divide " +
+                                    (g.uchan ? "tokens " : "channels ") + std::to_string(g.rowlen));
+  if (g.transform == T_HADAMARD && (C & (C - 1)))
+    return fail(KVC_ERR_CONFIG, "hadamard_over_channels needs power-of-two channels, got " + std::to_string(C));
+  if (g.transform == T_HADAMARD && C > 1024) return fail(KVC_ERR_CONFIG, "hadamard supports channels <= 1024");
+  if (C > 16384) return fail(KVC_ERR_CONFIG, "channels > 16384 unsupported");
+  if (g.uchan && (int64_t)g.group * C * 5 > 200 * 1024)
+    return fail(KVC_ERR_CONFIG, "uchan tile (group * channels) exceeds shared memory");
+  if ((g.quant == Q_MIXED || g.quant == Q_MIXLAYER) && g.LH > 32768)
+    return fail(KVC_ERR_CONFIG, "mixed quantization supports at most 32768 heads");
+  g.G = g.rowlen / g.group;
+  g.ngroups = g.E / g.group;
+  g.k_tok = g.quant == Q_MIXTOK ? (int64_t)std::ceil(rho * (double)T) : 0;
+  int64_t meta = 4 * g.ngroups;
+  g.meta_class_off = -1;
+  g.meta_affine_off = -1;
+  if (g.quant == Q_MIXED || g.quant == Q_MIXLAYER) {
+    g.meta_class_off = meta;
+    meta += (g.LH + 7) / 8;
+  }
+  if (g.transform == T_AFFINE) {
+    g.meta_affine_off = meta;
+    meta += 4 * g.LH * C;
+  }
+  p.meta_bytes = meta;
+  int wmax = (g.quant == Q_UNIFORM || g.quant == Q_UCHAN) ? g.bits : g.hi;
+  int64_t packed_cap = (g.E * wmax + 7) / 8 + 8;
+  p.max_blocks = g.codec == C_NONE ? 0 : (g.E + g.block - 1) / g.block + 1;
+  if (g.codec == C_ENTROPY) p.slot_bytes = align_up(4 * g.block + 16, 16);
+  else if (g.codec == C_RLE) p.slot_bytes = align_up(g.block + g.block / 128 + 16, 16);
+  p.payload_cap = g.codec == C_NONE ? packed_cap : p.max_blocks * p.slot_bytes;
+  p.scan_bytes = g.codec == C_NONE ? 0 : (int64_t)codec_scan_bytes(p.max_blocks);
+  int64_t off = 0;
+  p.ws_status = off; off += 256;
+  p.ws_streams = off; off += 256;
+  p.ws_heads = off; off = align_up(off + 16 * g.LH, 256);
+  p.ws_packed = off; off = align_up(off + (g.codec == C_NONE ? 0 : packed_cap), 256);
+  p.ws_slots = off; off = align_up(off + p.max_blocks * p.slot_bytes, 256);
+  p.ws_sizes = off; off = align_up(off + 8 * (p.max_blocks + 1), 256);
+  p.ws_scan = off; off = align_up(off + p.scan_bytes, 256);
+  p.ws_bytes = off;
+  snprintf(p.id, sizeof p.id, "%s", canon.c_str());
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    p.sm_count = 148;
+  }
+  kvc_plan* h = new kvc_plan;
+  h->p = p;
+  *out = h;
+  return KVC_OK;
+}
+
+int kvc_plan_destroy(kvc_plan* plan) {
+  delete plan;
+  return KVC_OK;
+}
+
+const char* kvc_plan_strategy_id(const kvc_plan* plan) { return plan ? plan->p.id : ""; }
+int64_t kvc_metadata_bytes(const kvc_plan* plan) { return plan ? plan->p.meta_bytes : -1; }
+int64_t kvc_payload_capacity(const kvc_plan* plan) { return plan ? plan->p.payload_cap : -1; }
+int64_t kvc_workspace_bytes(const kvc_plan* plan) { return plan ? plan->p.ws_bytes : -1; }
+int64_t kvc_max_blocks(const kvc_plan* plan) { return plan ? plan->p.max_blocks : -1; }
+
+int64_t kvc_static_payload_bytes(const kvc_plan* plan, const uint8_t* head_classes) {
+  if (!plan || plan->p.g.codec != C_NONE) return -1;
+  int n, w[2];
+  int64_t cnt[2];
+  host_streams(plan->p.g, head_classes, &n, w, cnt);
+  int64_t bytes = 0;
+  for (int i = 0; i < n; ++i) bytes += (cnt[i] * w[i] + 7) / 8;
+  return bytes;
+}
+
+int64_t kvc_num_blocks(const kvc_plan* plan, const uint8_t* head_classes) {
+  if (!plan) return -1;
+  if (plan->p.g.codec == C_NONE) return 0;
+  int n, w[2];
+  int64_t cnt[2];
+  host_streams(plan->p.g, head_classes, &n, w, cnt);
+  int64_t b = 0;
+  for (int i = 0; i < n; ++i) b += (cnt[i] + plan->p.g.block - 1) / plan->p.g.block;
+  return b;
+}
+
+static void fill_common(const Plan& p, double& hk, double& hc) {
+  hc = std::sqrt((double)p.g.C);
+  hk = std::ldexp(1.0 / hc, 896);
+}
+
+int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
+               uint64_t* block_offsets, void* workspace, void* stream) {
+  if (!plan) return fail(KVC_ERR_CONFIG, "plan is NULL");
+  const Plan& p = plan->p;
+  const Geo& g = p.g;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!kv || !payload || !metadata || !workspace) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  if (g.codec != C_NONE && !block_offsets) return fail(KVC_ERR_CONFIG, "block_offsets required for rle/entropy");
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  uint8_t* meta = reinterpret_cast<uint8_t*>(metadata);
+  uint32_t* status = reinterpret_cast<uint32_t*>(ws + p.ws_status);
+  StreamTab* st = reinterpret_cast<StreamTab*>(ws + p.ws_streams);
+  HeadEntry* heads = reinterpret_cast<HeadEntry*>(ws + p.ws_heads);
+  cudaError_t e;
+  if (g.quant == Q_MIXED || g.quant == Q_MIXLAYER) {
+    if (!head_classes) return fail(KVC_ERR_CONFIG, "mixed_head quantization needs head labels from classify_heads");
+    ClassBits cb;
+    memset(&cb, 0, sizeof cb);
+    for (int64_t i = 0; i < g.LH; ++i)
+      if (head_classes[i]) cb.b[i >> 3] |= (uint8_t)(0x80u >> (i & 7));
+    if ((e = launch_write_classmap(cb, meta + g.meta_class_off, (int)((g.LH + 7) / 8), s)) != cudaSuccess)
+      return cuda_fail(e, "classmap");
+  }
+  if ((e = launch_setup(g, meta, st, heads, s)) != cudaSuccess) return cuda_fail(e, "setup");
+  if (g.transform == T_AFFINE)
+    if ((e = launch_affine_calibrate(g, kv, meta, s)) != cudaSuccess) return cuda_fail(e, "affine");
+  EncArgs a;
+  memset(&a, 0, sizeof a);
+  a.g = g;
+  a.kv = kv;
+  a.packed = g.codec == C_NONE ? reinterpret_cast<uint8_t*>(payload) : ws + p.ws_packed;
+  a.meta = meta;
+  a.heads = heads;
+  a.st = st;
+  a.status = status;
+  fill_common(p, a.hk, a.hc);
+  for (int w = 1; w <= 8; ++w) a.rl[w] = 1.0f / (float)((1 << w) - 1);
+  const bool aligned = g.uchan ? (g.T % 8 == 0) : (g.C % 8 == 0);
+  if (!aligned) {
+    int64_t bytes = (g.E * ((g.quant == Q_UNIFORM || g.quant == Q_UCHAN) ? g.bits : g.hi) + 7) / 8 + 8;
+    if ((e = cudaMemsetAsync(a.packed, 0, (size_t)bytes, s)) != cudaSuccess) return cuda_fail(e, "memset");
+  }
+  if (fast128_applicable(g))
+    e = launch_encode_fast128(a, p.sm_count, s);
+  else
+    e = launch_encode_generic(a, s);
+  if (e != cudaSuccess) return cuda_fail(e, "encode kernel");
+  if (g.codec != C_NONE) {
+    CodecArgs c;
+    memset(&c, 0, sizeof c);
+    c.g = g;
+    c.st = st;
+    c.packed_in = a.packed;
+    c.payload_out = reinterpret_cast<uint8_t*>(payload);
+    c.offsets = block_offsets;
+    c.slots = ws + p.ws_slots;
+    c.sizes = reinterpret_cast<uint64_t*>(ws + p.ws_sizes);
+    c.scan_tmp = ws + p.ws_scan;
+    c.scan_bytes = (size_t)p.scan_bytes;
+    c.slot_bytes = p.slot_bytes;
+    c.max_blocks = p.max_blocks;
+    c.status = status;
+    if ((e = launch_codec_encode(c, p.sm_count, s)) != cudaSuccess) return cuda_fail(e, "codec encode");
+  }
+  return KVC_OK;
+}
+
+static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
+                       const uint64_t* block_offsets, void* out, int paged, const int32_t* block_table,
+                       int64_t page_tokens, int64_t layer_stride, void* workspace, void* stream) {
+  if (!plan) return fail(KVC_ERR_CONFIG, "plan is NULL");
+  const Plan& p = plan->p;
+  const Geo& g = p.g;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!payload || !metadata || !workspace || !out) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  if (g.codec != C_NONE && !block_offsets) return fail(KVC_ERR_CONFIG, "block_offsets required for rle/entropy");
+  if (paged && (!block_table || page_tokens < 1)) return fail(KVC_ERR_CONFIG, "paged decode needs a block table");
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const uint8_t* meta = reinterpret_cast<const uint8_t*>(metadata);
+  uint32_t* status = reinterpret_cast<uint32_t*>(ws + p.ws_status);
+  StreamTab* st = reinterpret_cast<StreamTab*>(ws + p.ws_streams);
+  HeadEntry* heads = reinterpret_cast<HeadEntry*>(ws + p.ws_heads);
+  cudaError_t e;
+  if ((e = launch_setup(g, meta, st, heads, s)) != cudaSuccess) return cuda_fail(e, "setup");
+  const uint8_t* packed = reinterpret_cast<const uint8_t*>(payload);
+  CodecArgs c;
+  memset(&c, 0, sizeof c);
+  c.g = g;
+  c.st = st;
+  c.payload_in = reinterpret_cast<const uint8_t*>(payload);
+  c.offsets_in = block_offsets;
+  c.packed_out = ws + p.ws_packed;
+  c.max_blocks = p.max_blocks;
+  c.payload_bytes = payload_bytes;
+  c.status = status;
+  if ((e = launch_codec_decode(c, p.sm_count, s)) != cudaSuccess) return cuda_fail(e, "codec decode");
+  if (g.codec != C_NONE) packed = ws + p.ws_packed;
+  DecArgs a;
+  memset(&a, 0, sizeof a);
+  a.g = g;
+  a.packed = packed;
+  a.meta = meta;
+  a.heads = heads;
+  a.st = st;
+  a.out = out;
+  a.status = status;
+  a.paged = paged;
+  a.block_table = block_table;
+  a.page_tokens = page_tokens;
+  a.layer_stride = layer_stride;
+  fill_common(p, a.hk, a.hc);
+  if (fast128_applicable(g))
+    e = launch_decode_fast128(a, p.sm_count, s);
+  else
+    e = launch_decode_generic(a, s);
+  if (e != cudaSuccess) return cuda_fail(e, "decode kernel");
+  return KVC_OK;
+}
+
+int kvc_decode(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
+               const uint64_t* block_offsets, void* out, void* workspace, void* stream) {
+  return decode_impl(plan, payload, payload_bytes, metadata, block_offsets, out, 0, nullptr, 0, 0, workspace, stream);
+}
+
+int kvc_decode_paged(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
+                     const uint64_t* block_offsets, void* page_base, const int32_t* block_table, int64_t page_tokens,
+                     int64_t layer_stride, void* workspace, void* stream) {
+  return decode_impl(plan, payload, payload_bytes, metadata, block_offsets, page_base, 1, block_table, page_tokens,
+                     layer_stride, workspace, stream);
+}
+
+int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_t* flags) {
+  if (!plan || !workspace || !flags) return fail(KVC_ERR_CONFIG, "NULL argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t* dev = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(workspace) + plan->p.ws_status);
+  uint32_t v = 0;
+  cudaError_t e = cudaMemcpyAsync(&v, dev, sizeof v, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dev, 0, sizeof v, s);
+  if (e != cudaSuccess) return cuda_fail(e, "read status");
+  *flags = v;
+  return KVC_OK;
+}
+
+}  // extern "C"

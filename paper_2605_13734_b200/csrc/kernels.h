@@ -1,0 +1,83 @@
+// Kernel argument blocks and launcher declarations.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kvc_internal.h"
+
+namespace kvc {
+
+struct EncArgs {
+  Geo g;
+  const void* kv;
+  uint8_t* packed;  // packed width streams (the payload for codec none)
+  uint8_t* meta;
+  const HeadEntry* heads;
+  const StreamTab* st;
+  uint32_t* status;
+  double hk, hc;    // hadamard: 2^896 * RN64(1/sqrt(C)), RN64(sqrt(C))
+  float rl[9];      // RN32(1 / (2^w - 1))
+};
+
+struct DecArgs {
+  Geo g;
+  const uint8_t* packed;
+  const uint8_t* meta;
+  const HeadEntry* heads;
+  const StreamTab* st;
+  void* out;
+  uint32_t* status;
+  double hk, hc;
+  int paged;
+  const int32_t* block_table;
+  int64_t page_tokens, layer_stride;
+};
+
+struct ClassBits {
+  uint8_t b[4096];
+};
+
+// Codec stage (operates on packed width streams).
+struct CodecArgs {
+  Geo g;
+  const StreamTab* st;
+  const uint8_t* packed_in;   // encode: packed streams
+  uint8_t* packed_out;        // decode: packed streams
+  const uint8_t* payload_in;  // decode: payload
+  uint8_t* payload_out;       // encode: payload
+  uint64_t* offsets;          // nblocks + 1
+  const uint64_t* offsets_in;
+  uint8_t* slots;             // encode scratch, slot_bytes per block
+  uint64_t* sizes;            // encode scratch, per block
+  void* scan_tmp;
+  size_t scan_bytes;
+  int64_t slot_bytes;
+  int64_t max_blocks;
+  int64_t payload_bytes;      // decode: caller's payload length
+  uint32_t* status;
+};
+
+__device__ __forceinline__ int64_t out_index(const DecArgs& a, int64_t lh, int64_t t, int64_t c) {
+  if (!a.paged) return (lh * a.g.T + t) * a.g.C + c;
+  const int64_t l = lh / a.g.H, h = lh - l * a.g.H;
+  const int64_t page = a.block_table[t / a.page_tokens];
+  return l * a.layer_stride + (page * a.page_tokens + t % a.page_tokens) * a.g.H * a.g.C + h * a.g.C + c;
+}
+
+cudaError_t launch_setup(const Geo& g, const uint8_t* meta, StreamTab* st, HeadEntry* heads, cudaStream_t s);
+cudaError_t launch_write_classmap(const ClassBits& cb, uint8_t* dst, int nbytes, cudaStream_t s);
+cudaError_t launch_affine_calibrate(const Geo& g, const void* kv, uint8_t* meta, cudaStream_t s);
+cudaError_t launch_encode_generic(const EncArgs& a, cudaStream_t s);
+cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s);
+
+// fast head_dim-128 per-token kernels (fast128.cu); return false if not applicable
+bool fast128_applicable(const Geo& g);
+cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_decode_fast128(const DecArgs& a, int sm_count, cudaStream_t s);
+
+// codec stage (codec.cu)
+size_t codec_scan_bytes(int64_t max_blocks);
+cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s);
+
+}  // namespace kvc

@@ -1,0 +1,152 @@
+// Exact-arithmetic device helpers.  Each reproduces one numpy expression of
+// the reference bit-for-bit while avoiding the slow B200 pipes we measured
+// (tools/ubench/pipes.cu: F2F f32<->f64 8-16/clk/SM, FRND 16, __fdiv_rn 3,
+// __ddiv_rn 1.2 vs 64 DADD / 128 FFMA per clk per SM).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "kvc_internal.h"
+
+namespace kvc {
+
+constexpr float kMagicRound = 12582912.0f;  // 1.5 * 2^23: x + M rounds x to an integer, half-to-even
+constexpr uint32_t kMagicBits = 0x4B400000u;
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+
+template <typename T>
+__device__ __forceinline__ float load_f32(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float load_f32<float>(const float* p, int64_t i) { return __ldg(p + i); }
+template <>
+__device__ __forceinline__ float load_f32<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return bf16_to_f32(__ldg(reinterpret_cast<const unsigned short*>(p) + i));
+}
+
+template <typename T>
+__device__ __forceinline__ void store_f32(T* p, int64_t i, float v);
+template <>
+__device__ __forceinline__ void store_f32<float>(float* p, int64_t i, float v) { p[i] = v; }
+template <>
+__device__ __forceinline__ void store_f32<__nv_bfloat16>(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+
+// ---------------------------------------------------------------------------
+// Hadamard (transforms.py:33-47, :62): fp64 butterfly, / RN64(sqrt n), -> f32.
+//
+// An fp32 bit pattern reinterpreted as the high/low words of a double is the
+// same value times 2^-896 for every finite input (zero, subnormal, normal):
+// the 8-bit exponent field lands in the 11-bit field unbiased by 896.  The
+// butterfly then runs on exactly scaled values (no rounding differs: tiny
+// sums are exact multiples of 2^-1045, representable even as fp64
+// subnormals), so the reference's fp64 results are reproduced without the
+// 16/clk/SM F2F.F64.F32 conversion.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double f32bits_scaled_f64(uint32_t f) {
+  return __hiloint2double((int)(((int)f >> 3) & (int)0x8FFFFFFF), (int)(f << 29));
+}
+
+// y = RN32(RN64(S / c)) where Sp = S * 2^-896 exactly, hk = 2^896 * RN64(1/c),
+// hc = c.  Fast path: RN64(S * RN64(1/c)) rounded to f32 with integer ops;
+// exact __ddiv_rn fallback when that product lies within 4 ulp64 of an f32
+// rounding boundary or outside the normal f32 range.
+__device__ __forceinline__ float hadamard_out(double Sp, double hk, double hc, uint32_t& flags) {
+  double q = Sp * hk;
+  uint32_t H = (uint32_t)__double2hiint(q), Lw = (uint32_t)__double2loint(q);
+  uint32_t m = Lw & 0x1FFFFFFFu;
+  uint32_t e = (H >> 20) & 0x7FFu;
+  if ((e - 897u) < 254u && (m - 0x0FFFFFFCu) > 8u) {
+    uint32_t t = __funnelshift_l(Lw, H, 3);
+    t = t - 0xC0000000u + (m > 0x10000000u ? 1u : 0u);
+    return __uint_as_float((t & 0x7FFFFFFFu) | (H & 0x80000000u));
+  }
+  if (((H & 0x7FFFFFFFu) | Lw) == 0u) return __uint_as_float(H & 0x80000000u);  // signed zero
+  double S = Sp * 0x1p896;
+  float y = __double2float_rn(__ddiv_rn(S, hc));
+  if (!isfinite(y)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// Group scale (quantize.py:146): float16(float64(d) / levels), d = fp32 max-min.
+// d/levels never rounds onto an fp16 midpoint through fp64 unless it is one
+// exactly, so this equals RN16(d/levels); computed in fp32 and checked for
+// proximity to an fp16 boundary (relative 2^-20 vs an error of 2^-23).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ __half scale16_exact(float d, float levels, float rl) {
+  float q = __fmul_rn(d, rl);
+  __half a = __float2half_rn(__fmul_rn(q, 1.00000095367431640625f));
+  __half b = __float2half_rn(__fmul_rn(q, 0.99999904632568359375f));
+  if (__half_as_ushort(a) == __half_as_ushort(b)) return a;
+  return __double2half(__ddiv_rn((double)d, (double)levels));
+}
+
+// Per-group quantizer state (quantize.py:146-154).
+struct GroupQ {
+  float s, z, r, lv;
+  int mode;  // 0 fast, 1 all-zero symbols (scale 0), 2 exact slow path (inf scale/zero)
+};
+
+__device__ __forceinline__ GroupQ group_setup(float mn, float mx, int w, float rl, __half& s16, __half& z16,
+                                              uint32_t& flags) {
+  GroupQ q;
+  q.lv = (float)((1 << w) - 1);
+  float d = __fsub_rn(mx, mn);
+  s16 = scale16_exact(d, q.lv, rl);
+  z16 = __float2half_rn(mn);
+  q.s = __half2float(s16);
+  q.z = __half2float(z16);
+  if (!(q.s > 0.0f)) {
+    q.mode = 1;
+    q.r = 0.0f;
+  } else if (isinf(q.s) || isinf(q.z)) {
+    q.mode = 2;
+    q.r = 0.0f;
+    flags |= KVC_FLAG_FP16_RANGE;
+  } else {
+    q.mode = 0;
+    q.r = __frcp_rn(q.s);
+  }
+  if (isinf(q.z)) flags |= KVC_FLAG_FP16_RANGE;
+  return q;
+}
+
+// rint(fp32((v - z) / s)) clipped to [0, levels] (quantize.py:152-154).
+// Reciprocal + two FMAs reproduce the IEEE quotient (exhaustively checked
+// over all fp16 scales: tools/numerics/markstein_check.c); the pre-clamp at
+// 512 keeps the residual finite; rint is the 1.5*2^23 magic add.
+__device__ __forceinline__ uint32_t quant_fast(float v, const GroupQ& q) {
+  float d = __fsub_rn(v, q.z);
+  float q0 = fminf(__fmul_rn(d, q.r), 512.0f);
+  float e = __fmaf_rn(-q0, q.s, d);
+  float q1 = __fmaf_rn(e, q.r, q0);
+  float c = fminf(fmaxf(q1, 0.0f), q.lv);
+  return __float_as_uint(__fadd_rn(c, kMagicRound)) - kMagicBits;
+}
+
+__device__ __forceinline__ uint32_t quant_one(float v, const GroupQ& q) {
+  if (q.mode == 0) return quant_fast(v, q);
+  if (q.mode == 1) return 0u;
+  float r = rintf(__fdiv_rn(__fsub_rn(v, q.z), q.s));
+  r = fminf(fmaxf(r, 0.0f), q.lv);  // NaN -> 0 like numpy's uint8 cast on x86
+  return (uint32_t)r;
+}
+
+// dequantize (quantize.py:178): zero + symbol*scale, unfused.
+__device__ __forceinline__ float dequant(uint32_t sym, float s, float z) {
+  return __fadd_rn(z, __fmul_rn(__uint_as_float(0x4B000000u | sym) - 8388608.0f, s));
+}
+
+// read a w-bit MSB-first symbol starting at absolute bit p
+__device__ __forceinline__ uint32_t read_sym(const uint8_t* buf, int64_t p, int w) {
+  int64_t byte = p >> 3;
+  int sh = (int)(p & 7);
+  uint32_t v = (uint32_t)buf[byte] << 8;
+  if (sh + w > 8) v |= buf[byte + 1];
+  return (v >> (16 - sh - w)) & ((1u << w) - 1u);
+}
+
+}  // namespace kvc

@@ -1,0 +1,93 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol
+include/kvc.h declares, and plan creation validates like the reference."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2605_13734_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_13734_b200._build import build
+
+    build()
+    return N.lib()
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "kvc.h")).read()
+    return sorted(set(re.findall(r"\b(kvc_[a-z_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(lib):
+    syms = header_symbols()
+    assert set(syms) == set(N.EXPORTS)
+    for s in syms:
+        assert hasattr(lib, s), s
+
+
+def _plan(lib, sid, shape=(2, 4, 64, 128), block=4096):
+    h = ctypes.c_void_p()
+    o = N.KvcOptions()
+    o.block_symbols = block
+    rc = lib.kvc_plan_create(ctypes.byref(h), sid.encode(), *shape, ctypes.byref(o))
+    return rc, h
+
+
+def test_plan_sizes(lib):
+    rc, h = _plan(lib, "t=hadamard;q=uniform,b=4,g=32;c=none")
+    assert rc == 0
+    L, H, T, C = 2, 4, 64, 128
+    assert lib.kvc_metadata_bytes(h) == 4 * L * H * T * C // 32
+    assert lib.kvc_static_payload_bytes(h, None) == L * H * T * C * 4 // 8
+    assert lib.kvc_plan_strategy_id(h).decode() == "t=hadamard;q=uniform,b=4,g=32;c=none"
+    lib.kvc_plan_destroy(h)
+    rc, h = _plan(lib, " t=identity;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=entropy\n", block=512)
+    assert rc == 0
+    assert lib.kvc_metadata_bytes(h) == 4 * L * H * T * C // 32 + 1
+    cls = (ctypes.c_uint8 * 8)(1, 0, 0, 0, 0, 0, 0, 1)
+    assert lib.kvc_num_blocks(h, cls) == (2 * T * C + 511) // 512 + (6 * T * C + 511) // 512
+    lib.kvc_plan_destroy(h)
+
+
+@pytest.mark.parametrize("text", [
+    "t=identity;q=uniform,b=4,g=32",
+    "t=identity;q=uniform,b=4,g=32;c=none;extra=1",
+    "t=fourier;q=uniform,b=4,g=32;c=none",
+    "x=identity;q=uniform,b=4,g=32;c=none",
+    "t=identity;q=uniform,b=4,g=32;c=zstd",
+    "t=identity;q=vector,b=4,g=32;c=none",
+    "t=identity;q=uniform,b=4;c=none",
+    "t=identity;q=uniform,b=4,g=32,rho=0.5;c=none",
+    "t=identity;q=mixed,hi=8,lo=2,g=32;c=none",
+    "t=identity;q=uniform,b4,g=32;c=none",
+    "t=identity;q=uniform,b=four,g=32;c=none",
+    "t=identity;q=uniform,b=9,g=32;c=none",
+    "t=identity;q=mixed,hi=2,lo=4,g=32,rho=0.25;c=none",
+    "t=identity;q=mixed,hi=8,lo=2,g=32,rho=1.5;c=none",
+    "t=identity;q=uniform,b=4,g=48;c=none",
+])
+def test_rejects_like_reference(lib, text):
+    """Malformed ids from test_strategy.py:179-197 plus config validation."""
+    rc, h = _plan(lib, text)
+    assert rc == N.KVC_ERR_CONFIG, text
+    with pytest.raises(ValueError):
+        N.check(rc)
+
+
+def test_hadamard_needs_power_of_two(lib):
+    rc, _ = _plan(lib, "t=hadamard;q=uniform,b=4,g=16;c=none", shape=(1, 1, 2, 48))
+    assert rc == N.KVC_ERR_CONFIG
+    assert "power-of-two" in lib.kvc_last_error().decode()
+
+
+def test_canonical_rho_repr(lib):
+    rc, h = _plan(lib, "t=delta;q=mixed,hi=4,lo=3,g=64,rho=0.1250;c=rle", shape=(1, 1, 4, 64))
+    assert rc == 0
+    assert lib.kvc_plan_strategy_id(h).decode() == "t=delta;q=mixed,hi=4,lo=3,g=64,rho=0.125;c=rle"
