@@ -97,7 +97,10 @@ int64_t kvc_num_blocks(const kvc_plan* plan, const uint8_t* head_classes);
 int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
                uint64_t* block_offsets, void* workspace, void* stream);
 
-/* Decode into a contiguous (L,H,T,C) tensor of the plan's out_dtype. */
+/* Decode into a contiguous (L,H,T,C) tensor of the plan's out_dtype.
+ * `payload_bytes` is the received payload length (checked like the
+ * reference's trailing-byte rule, codecs.py:412-413 / :429-430); pass -1 for a
+ * device-resident blob whose length is block_offsets[nblocks]. */
 int kvc_decode(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
                const uint64_t* block_offsets, void* out, void* workspace, void* stream);
 
@@ -113,6 +116,16 @@ int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_
 
 const char* kvc_last_error(void);
 const char* kvc_version(void);
+
+/* Per-kernel timing (the native side of the StageTimer hook, compress.py:43-48).
+ * When enabled, every kernel the library launches on the calling thread is
+ * bracketed by CUDA events on its stream.  kvc_profile_collect synchronises,
+ * accumulates elapsed milliseconds per kernel name into `ms` / `launches`
+ * (up to `cap` distinct names, order of first launch), writes the names
+ * (NUL-separated) into `names` (size `names_cap`), clears the record and
+ * returns the number of names. */
+int kvc_profile_enable(int on);
+int kvc_profile_collect(char* names, int64_t names_cap, double* ms, int64_t* launches, int cap);
 
 #ifdef __cplusplus
 }

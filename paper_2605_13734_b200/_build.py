@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libkvc.so")
-SOURCES = ["api.cu", "generic.cu", "fast128.cu", "codec.cu"]
+SOURCES = ["api.cu", "generic.cu", "fast128.cu", "codec.cu", "profile.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -25,7 +25,7 @@ FLAGS = [
 
 
 def _compile(src: str) -> str:
-    out = os.path.join(OBJ, src.replace(".cu", ".o"))
+    out = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
     deps = [path] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "kvc.h"))

@@ -37,6 +37,8 @@ EXPORTS = (
     "kvc_read_status",
     "kvc_last_error",
     "kvc_version",
+    "kvc_profile_enable",
+    "kvc_profile_collect",
 )
 
 
@@ -93,6 +95,10 @@ def lib() -> ctypes.CDLL:
     L.kvc_last_error.restype = ctypes.c_char_p
     L.kvc_version.argtypes = []
     L.kvc_version.restype = ctypes.c_char_p
+    L.kvc_profile_enable.argtypes = [I32]
+    L.kvc_profile_enable.restype = I32
+    L.kvc_profile_collect.argtypes = [ctypes.c_char_p, I64, P, P, I32]
+    L.kvc_profile_collect.restype = I32
     _lib = L
     return L
 
@@ -117,3 +123,20 @@ def raise_for_flags(flags: int, decoding: bool) -> None:
         raise ValueError("values must be finite")
     if flags & FLAG_NONFINITE_TRANSFORM:
         raise ValueError("values must be finite")
+
+
+def profile_enable(on: bool) -> None:
+    lib().kvc_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict:
+    """{kernel name: (total ms, launches)} since the last collect (syncs)."""
+    import numpy as np
+
+    cap = 64
+    names = ctypes.create_string_buffer(4096)
+    ms = np.zeros(cap, dtype=np.float64)
+    cnt = np.zeros(cap, dtype=np.int64)
+    n = lib().kvc_profile_collect(names, 4096, ms.ctypes.data_as(ctypes.c_void_p), cnt.ctypes.data_as(ctypes.c_void_p), cap)
+    keys = names.raw.split(b"\0")[:n]
+    return {k.decode(): (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}

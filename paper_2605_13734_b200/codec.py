@@ -185,14 +185,16 @@ class KVCodec:
 
     # ------------------------------------------------------------- decode
     def decode(self, blob: DeviceBlob, out: torch.Tensor | None = None,
-               stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+               stream: torch.cuda.Stream | None = None, device_length: bool = False) -> torch.Tensor:
+        """Decode a blob.  device_length=True takes the payload length from the
+        device offset table (no host sync; for device-resident blobs)."""
         if out is None:
             out = torch.empty(self.shape, dtype=self.out_dtype, device=self.device)
         if out.dtype != self.out_dtype or tuple(out.shape) != self.shape or not out.is_contiguous():
             raise ValueError("bad output tensor")
         if blob.metadata.numel() != self.metadata_bytes:
             raise N.CodecError(f"metadata is {blob.metadata.numel()} bytes, expected {self.metadata_bytes}")
-        nbytes = blob.payload_nbytes()
+        nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
         N.check(
             self._lib.kvc_decode(
                 self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),

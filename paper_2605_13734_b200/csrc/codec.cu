@@ -13,6 +13,7 @@
 
 #include "kernels.h"
 #include "numerics.cuh"
+#include "profile.h"
 
 namespace kvc {
 
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(128) k_rc_decode(CodecArgs a) {
   const int64_t start = (b - st.first_block[si]) * a.g.block;
   const int64_t n = min(a.g.block, st.count[si] - start);
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  if (o1 < o0 || (int64_t)o1 > a.payload_bytes) {
+  if (o1 < o0 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
   const int64_t n = min(a.g.block, st.count[si] - start);
   const int64_t want = (n * w + 7) / 8;
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  if (o1 < o0 || (int64_t)o1 > a.payload_bytes) {
+  if (o1 < o0 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
@@ -494,18 +495,21 @@ __global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
 __global__ void k_check_payload(CodecArgs a) {
   const StreamTab& st = *a.st;
   if (a.g.codec == C_NONE) {
-    if (a.payload_bytes != st.packed_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
+    if (a.payload_bytes >= 0 && a.payload_bytes != st.packed_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
-  if (a.offsets_in[0] != 0 || (int64_t)a.offsets_in[st.nblocks] != a.payload_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
+  if (a.offsets_in[0] != 0) atomicOr(a.status, KVC_FLAG_CODEC);
+  if (a.payload_bytes >= 0 && (int64_t)a.offsets_in[st.nblocks] != a.payload_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
 }
 
 template <int W>
 void launch_rc_encode_w(const CodecArgs& a, unsigned grid, cudaStream_t s) {
+  ProfScope ps("rc_encode", s);
   k_rc_encode<W><<<grid, 128, 0, s>>>(a);
 }
 template <int W>
 void launch_rc_decode_w(const CodecArgs& a, unsigned grid, cudaStream_t s) {
+  ProfScope ps("rc_decode", s);
   k_rc_decode<W><<<grid, 128, 0, s>>>(a);
 }
 
@@ -542,21 +546,29 @@ cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s
     if (used[7]) launch_rc_encode_w<7>(a, grid, s);
     if (used[8]) launch_rc_encode_w<8>(a, grid, s);
   } else {
+    ProfScope ps("rle_encode", s);
     k_rle_encode<<<grid, 128, 0, s>>>(a);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   size_t tmp = a.scan_bytes;
+  {
+  ProfScope ps("offset_scan", s);
   e = cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.sizes, a.offsets, (int)(a.max_blocks + 1), s);
+  }
   if (e != cudaSuccess) return e;
   const unsigned ggrid = (unsigned)((a.max_blocks * 32 + 255) / 256 + 1);
+  ProfScope ps("gather", s);
   k_gather<<<ggrid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s) {
   (void)sm_count;
-  k_check_payload<<<1, 1, 0, s>>>(a);
+  {
+    ProfScope ps("check_payload", s);
+    k_check_payload<<<1, 1, 0, s>>>(a);
+  }
   if (a.g.codec == C_NONE) return cudaGetLastError();
   const unsigned grid = (unsigned)((a.max_blocks + 127) / 128 + 1);
   bool used[9];
@@ -571,6 +583,7 @@ cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s
     if (used[7]) launch_rc_decode_w<7>(a, grid, s);
     if (used[8]) launch_rc_decode_w<8>(a, grid, s);
   } else {
+    ProfScope ps("rle_decode", s);
     k_rle_decode<<<grid, 128, 0, s>>>(a);
   }
   return cudaGetLastError();

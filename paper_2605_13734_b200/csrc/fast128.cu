@@ -1,7 +1,653 @@
-// placeholder: replaced by the fused head_dim-128 kernels
+// Fused head_dim-128 per-token kernels: the hot path for bf16 serving caches.
+//
+// Encode (kernel 1 of the north star): one CTA streams tiles of 64 token rows
+// (16 KB bf16) through a 4-deep TMA ring (cp.async.bulk.tensor, 128B swizzle,
+// mbarrier completion).  Two threads own a row, one 64-channel half each:
+//   transform -> group min/max -> fp16 scale/zero -> symbols -> MSB-first
+//   bit packing straight into the width stream (codecs.py:79-87, :339-345).
+// Hadamard runs as a float64 butterfly in registers in the reference's stage
+// order (h = 1..32 in-thread, h = 64 as one shuffle exchange), then the exact
+// RN32(RN64(S / sqrt 128)) rounding of numerics.cuh.
+// Decode (kernel 3): packed stream -> dequantize -> inverse transform (fp32,
+// within the reference's tolerance) -> bf16 rows, contiguous or paged.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
 #include "kernels.h"
+#include "numerics.cuh"
+#include "profile.h"
+#include "rowpos.cuh"
+
 namespace kvc {
-bool fast128_applicable(const Geo&) { return false; }
-cudaError_t launch_encode_fast128(const EncArgs&, int, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t launch_decode_fast128(const DecArgs&, int, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int kThreads = 128;            // 64 rows per tile
+constexpr int kRows = kThreads / 2;
+constexpr int kStages = 4;
+constexpr int kTileBytes = kThreads * 128;  // one 128 B half-row per thread
+constexpr int kSmemBytes = kStages * kTileBytes + 1024 + 64;
+
+enum Mode { M_IDENTITY = 0, M_DELTA = 1, M_HADAMARD = 2, M_AFFINE = 3 };
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ----------------------------------------------------------- bit packing
+// Pack 32 symbols (low byte of the magic-rounded floats) at width W,
+// MSB-first (codecs.py:79-87), and store the 4W bytes at dst (4-byte aligned).
+template <int W>
+__device__ __forceinline__ void pack32_store(const float* q, uint8_t* dst) {
+  uint32_t be[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) be[k] = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t s = __float_as_uint(q[i]) & ((1u << W) - 1u);
+    const int p = i * W, k = p >> 5, off = p & 31;
+    if (off + W <= 32) {
+      be[k] |= s << (32 - off - W);
+    } else {
+      be[k] |= s >> (off + W - 32);
+      be[k + 1] |= s << (64 - off - W);
+    }
+  }
+  uint32_t wd[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) wd[k] = __byte_perm(be[k], 0, 0x0123);
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 4) *reinterpret_cast<uint4*>(dst + 4 * k) = make_uint4(wd[k], wd[k + 1], wd[k + 2], wd[k + 3]);
+  } else if constexpr (W % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 2) *reinterpret_cast<uint2*>(dst + 4 * k) = make_uint2(wd[k], wd[k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) reinterpret_cast<uint32_t*>(dst)[k] = wd[k];
+  }
+}
+
+__device__ __forceinline__ void pack32_dispatch(int w, const float* q, uint8_t* dst) {
+  switch (w) {
+    case 1: pack32_store<1>(q, dst); break;
+    case 2: pack32_store<2>(q, dst); break;
+    case 3: pack32_store<3>(q, dst); break;
+    case 4: pack32_store<4>(q, dst); break;
+    case 5: pack32_store<5>(q, dst); break;
+    case 6: pack32_store<6>(q, dst); break;
+    case 7: pack32_store<7>(q, dst); break;
+    default: pack32_store<8>(q, dst); break;
+  }
+}
+
+// Unpack 32 symbols of width W from src (4-byte aligned) into floats.
+template <int W>
+__device__ __forceinline__ void unpack32(const uint8_t* src, float* v) {
+  uint32_t be[W];
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 4) {
+      uint4 t = *reinterpret_cast<const uint4*>(src + 4 * k);
+      be[k] = t.x; be[k + 1] = t.y; be[k + 2] = t.z; be[k + 3] = t.w;
+    }
+  } else if constexpr (W % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 2) {
+      uint2 t = *reinterpret_cast<const uint2*>(src + 4 * k);
+      be[k] = t.x; be[k + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) be[k] = reinterpret_cast<const uint32_t*>(src)[k];
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) be[k] = __byte_perm(be[k], 0, 0x0123);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int p = i * W, k = p >> 5, off = p & 31;
+    uint32_t s;
+    if (off + W <= 32) {
+      s = (be[k] >> (32 - off - W)) & ((1u << W) - 1u);
+    } else {
+      s = ((be[k] << (off + W - 32)) | (be[k + 1] >> (64 - off - W))) & ((1u << W) - 1u);
+    }
+    v[i] = __uint_as_float(0x4B000000u | s) - 8388608.0f;
+  }
+}
+
+__device__ __forceinline__ void unpack32_dispatch(int w, const uint8_t* src, float* v) {
+  switch (w) {
+    case 1: unpack32<1>(src, v); break;
+    case 2: unpack32<2>(src, v); break;
+    case 3: unpack32<3>(src, v); break;
+    case 4: unpack32<4>(src, v); break;
+    case 5: unpack32<5>(src, v); break;
+    case 6: unpack32<6>(src, v); break;
+    case 7: unpack32<7>(src, v); break;
+    default: unpack32<8>(src, v); break;
+  }
+}
+
+// ------------------------------------------------------------ group stats
+// Quantize the thread's 64 values (two chunks of 32 at channel bases cb0,
+// cb1), group size G in {8,16,32,64,128}; `xchg` = the partner thread holds
+// the other half of a 64/128 group (hadamard layout or G = 128).
+template <int G>
+__device__ __forceinline__ void quantize64(float* y, int cb0, int cb1, int w, float rl, int64_t grow,
+                                           __half* scales, __half* zeros, bool hadlayout, int half,
+                                           uint32_t& flags) {
+  if constexpr (G <= 32) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll
+      for (int j = 0; j < 32 / G; ++j) {
+        float* yy = y + c * 32 + j * G;
+        float mn = yy[0], mx = yy[0];
+#pragma unroll
+        for (int i = 1; i < G; ++i) {
+          mn = fminf(mn, yy[i]);
+          mx = fmaxf(mx, yy[i]);
+        }
+        __half s16, z16;
+        GroupQ q = group_setup(mn, mx, w, rl, s16, z16, flags);
+        const int64_t gi = grow + ((c ? cb1 : cb0) + j * G) / G;
+        if (scales) {
+          scales[gi] = s16;
+          zeros[gi] = z16;
+        }
+        if (q.mode == 0) {
+#pragma unroll
+          for (int i = 0; i < G; ++i) yy[i] = quant_magic(yy[i], q);
+        } else {
+#pragma unroll
+          for (int i = 0; i < G; ++i) yy[i] = __uint_as_float(kMagicBits + quant_one(yy[i], q));
+        }
+      }
+    }
+  } else {
+    // G = 64 or 128: stats over both chunks and/or the partner thread
+    float mn0 = y[0], mx0 = y[0], mn1 = y[32], mx1 = y[32];
+#pragma unroll
+    for (int i = 1; i < 32; ++i) {
+      mn0 = fminf(mn0, y[i]); mx0 = fmaxf(mx0, y[i]);
+      mn1 = fminf(mn1, y[32 + i]); mx1 = fmaxf(mx1, y[32 + i]);
+    }
+    float gmn[2], gmx[2];
+    if (G == 128) {
+      float mn = fminf(mn0, mn1), mx = fmaxf(mx0, mx1);
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      gmn[0] = gmn[1] = mn;
+      gmx[0] = gmx[1] = mx;
+    } else if (!hadlayout) {  // natural layout: both chunks form the group
+      gmn[0] = gmn[1] = fminf(mn0, mn1);
+      gmx[0] = gmx[1] = fmaxf(mx0, mx1);
+    } else {  // hadamard layout: chunk c of both threads forms group c
+      gmn[0] = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 1));
+      gmx[0] = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      gmn[1] = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, 1));
+      gmx[1] = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      __half s16, z16;
+      GroupQ q = group_setup(gmn[c], gmx[c], w, rl, s16, z16, flags);
+      const int64_t gi = grow + (c ? cb1 : cb0) / G;
+      // one writer per group
+      const bool writer = (G == 128) ? (half == 0 && c == 0) : (!hadlayout ? c == 0 : (half == c));
+      if (writer && scales) {
+        scales[gi] = s16;
+        zeros[gi] = z16;
+      }
+      float* yy = y + c * 32;
+      if (q.mode == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) yy[i] = quant_magic(yy[i], q);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) yy[i] = __uint_as_float(kMagicBits + quant_one(yy[i], q));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ encode kernel
+template <int MODE, int G>
+__global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DELTA) ? 3 : 4)
+    k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + kStages * kTileBytes);
+  const Geo& g = a.g;
+  const int64_t nrows = g.LH * g.T;
+  const int64_t ntiles = (nrows + kRows - 1) / kRows;
+  const int tid = threadIdx.x, half = tid & 1;
+  const uint32_t sw = (uint32_t)(tid & 7);
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < ntiles) {
+        mbar_expect_tx(&full[s], kTileBytes);
+        tma_load_2d(tiles + s * kTileBytes, &tmap, 0, (int)(tile * kThreads), &full[s]);
+      }
+    }
+  }
+  __half* scales = reinterpret_cast<__half*>(a.meta);
+  __half* zeros = scales + g.ngroups;
+  uint32_t flags = 0;
+  float nanacc = 0.0f;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % kStages;
+    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
+    const uint8_t* tb = tiles + s * kTileBytes;
+    uint32_t wv[32];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint4 c = *reinterpret_cast<const uint4*>(tb + tid * 128 + (((uint32_t)k ^ sw) << 4));
+      wv[4 * k] = c.x; wv[4 * k + 1] = c.y; wv[4 * k + 2] = c.z; wv[4 * k + 3] = c.w;
+    }
+    const int64_t row = tile * kRows + (tid >> 1);
+    const bool valid = row < nrows;
+    const int64_t lh = valid ? row / g.T : 0;
+    const int64_t t = valid ? row - lh * g.T : 0;
+    uint32_t pv[32];  // delta: previous row's half
+    if (MODE == M_DELTA) {
+      if (tid >= 2) {
+        const uint32_t psw = (uint32_t)((tid - 2) & 7);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint4 c = *reinterpret_cast<const uint4*>(tb + (tid - 2) * 128 + (((uint32_t)k ^ psw) << 4));
+          pv[4 * k] = c.x; pv[4 * k + 1] = c.y; pv[4 * k + 2] = c.z; pv[4 * k + 3] = c.w;
+        }
+      } else if (valid && t > 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + (row - 1) * 128 + half * 64);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint4 c = __ldg(src + k);
+          pv[4 * k] = c.x; pv[4 * k + 1] = c.y; pv[4 * k + 2] = c.z; pv[4 * k + 3] = c.w;
+        }
+      }
+    }
+    __syncthreads();  // every thread has its half-row in registers: slot s is free
+    if (tid == 0) {
+      const int64_t next = tile + (int64_t)kStages * gridDim.x;
+      if (next < ntiles) {
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], kTileBytes);
+        tma_load_2d(tiles + s * kTileBytes, &tmap, 0, (int)(next * kThreads), &full[s]);
+      }
+    }
+    // invalid tail rows run the same code (shuffles need the full warp) but
+    // store nothing
+
+    float y[64];
+    int cb0, cb1;
+    bool hadlayout = false;
+    if (MODE == M_HADAMARD) {
+      double f[64];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        f[2 * j] = f32bits_scaled_f64(wv[j] << 16);
+        f[2 * j + 1] = f32bits_scaled_f64(wv[j] & 0xFFFF0000u);
+      }
+      // stages h = 1..32 (transforms.py:41-46 order), in registers
+#pragma unroll
+      for (int h = 1; h < 64; h <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          if ((i & h) == 0) {
+            const double u = f[i], v = f[i + h];
+            f[i] = u + v;
+            f[i + h] = u - v;
+          }
+        }
+      }
+      // stage h = 64 across the thread pair: A (half 0) keeps outputs 0..31 and
+      // 64..95, B keeps 32..63 and 96..127.
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const double send = half ? f[k] : f[32 + k];
+        const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(send), 1);
+        const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(send), 1);
+        const double r = __hiloint2double(hi, lo);
+        if (!half) {
+          const double u = f[k];
+          f[k] = u + r;
+          f[32 + k] = u - r;
+        } else {
+          const double v = f[32 + k];
+          f[k] = r + v;
+          f[32 + k] = r - v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) y[i] = hadamard_out(f[i], a.hk, a.hc, flags);
+      cb0 = 32 * half;
+      cb1 = 64 + 32 * half;
+      hadlayout = true;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        y[2 * j] = __uint_as_float(wv[j] << 16);
+        y[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
+      }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) nanacc = __fmaf_rn(y[i], 0.0f, nanacc);
+      if (MODE == M_DELTA && t > 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          y[2 * j] = __fsub_rn(y[2 * j], __uint_as_float(pv[j] << 16));
+          y[2 * j + 1] = __fsub_rn(y[2 * j + 1], __uint_as_float(pv[j] & 0xFFFF0000u));
+        }
+      }
+      if (MODE == M_AFFINE) {
+        const uint4* mu = reinterpret_cast<const uint4*>(a.meta + g.meta_affine_off + (lh * 128 + half * 64) * 2);
+        const uint4* sc = reinterpret_cast<const uint4*>(a.meta + g.meta_affine_off + (g.LH * 128 + lh * 128 + half * 64) * 2);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint4 m4 = __ldg(mu + k), s4 = __ldg(sc + k);
+          const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w}, sw4[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 mf = __half22float2(*reinterpret_cast<const __half2*>(&mw[q]));
+            const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sw4[q]));
+            const int i = 8 * k + 2 * q;
+            y[i] = __fmul_rn(__fsub_rn(y[i], mf.x), sf.x);
+            y[i + 1] = __fmul_rn(__fsub_rn(y[i + 1], mf.y), sf.y);
+          }
+        }
+      }
+      if (MODE == M_DELTA || MODE == M_AFFINE) {
+        float chk = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
+        if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+      }
+      cb0 = 64 * half;
+      cb1 = 64 * half + 32;
+    }
+
+    int w;
+    int64_t bit;
+    token_row_pos(g, a.heads, lh, t, w, bit);
+    quantize64<G>(y, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros, hadlayout, half, flags);
+    if (valid) {
+      uint8_t* out = a.packed + (bit >> 3);
+      pack32_dispatch(w, y, out + cb0 * w / 8);
+      pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+    }
+  }
+  if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
+  flags = __syncthreads_or(flags);
+  if (tid == 0 && flags) atomicOr(a.status, flags);
+}
+
+// ------------------------------------------------------------ decode kernel
+template <int G>
+__device__ __forceinline__ void dequant64(float* y, int cb0, int cb1, int64_t row, const __half* scales,
+                                          const __half* zeros) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int cb = c ? cb1 : cb0;
+#pragma unroll
+    for (int j = 0; j < (G < 32 ? 32 / G : 1); ++j) {
+      const int64_t gi = row * (128 / G) + (cb + j * G) / G;
+      const float s = __half2float(scales[gi]), z = __half2float(zeros[gi]);
+      constexpr int n = G < 32 ? G : 32;
+#pragma unroll
+      for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fadd_rn(z, __fmul_rn(y[32 * c + j * n + i], s));
+    }
+  }
+}
+
+template <int MODE, typename Tout, int G>
+__global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
+  const Geo& g = a.g;
+  const int64_t nrows = g.LH * g.T;
+  const int64_t ntiles = (nrows + kRows - 1) / kRows;
+  const int tid = threadIdx.x, half = tid & 1;
+  const __half* scales = reinterpret_cast<const __half*>(a.meta);
+  const __half* zeros = scales + g.ngroups;
+  uint32_t flags = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * kRows + (tid >> 1);
+    const bool valid = row0 < nrows;
+    const int64_t row = valid ? row0 : nrows - 1;  // tail lanes mirror a real row, store nothing
+    const int64_t lh = row / g.T;
+    const int64_t t = row - lh * g.T;
+    int w;
+    int64_t bit;
+    token_row_pos(g, a.heads, lh, t, w, bit);
+    constexpr bool had = MODE == M_HADAMARD;
+    const int cb0 = had ? 32 * half : 64 * half;
+    const int cb1 = had ? 64 + 32 * half : 64 * half + 32;
+    const uint8_t* src = a.packed + (bit >> 3);
+    float y[64];
+    unpack32_dispatch(w, src + cb0 * w / 8, y);
+    unpack32_dispatch(w, src + cb1 * w / 8, y + 32);
+    dequant64<G>(y, cb0, cb1, row, scales, zeros);
+    if (MODE == M_HADAMARD) {
+      // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
+      // (decode is held to tolerance): in-thread stages over channel bits
+      // 0-4 and 6, one pair exchange for bit 5.
+#pragma unroll
+      for (int h = 1; h < 32; h <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          if ((i & h) == 0) {
+            const float u = y[i], v = y[i + h];
+            y[i] = u + v;
+            y[i + h] = u - v;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float u = y[i], v = y[32 + i];
+        y[i] = u + v;
+        y[32 + i] = u - v;
+      }
+      // afterwards A (half 0) holds channels 0..63 and B 64..127
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float send = half ? y[k] : y[32 + k];
+        const float r = __shfl_xor_sync(0xffffffffu, send, 1);
+        if (!half) {
+          const float u = y[k];
+          y[k] = u + r;
+          y[32 + k] = u - r;
+        } else {
+          const float v = y[32 + k];
+          y[k] = r + v;
+          y[32 + k] = r - v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) y[i] = __fmul_rn(y[i], 0.08838834764831845f);  // RN32(1/sqrt(128))
+    } else if (MODE == M_AFFINE) {
+      const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
+      const __half* scl = mu + g.LH * 128;
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
+    }
+    if (!valid) continue;
+    float chk = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
+    if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+    Tout* out = reinterpret_cast<Tout*>(a.out) + out_index(a, lh, t, 64 * half);
+    if constexpr (sizeof(Tout) == 2) {
+      uint4* o = reinterpret_cast<uint4*>(out);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t p[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __nv_bfloat162 b = __floats2bfloat162_rn(y[8 * k + 2 * q], y[8 * k + 2 * q + 1]);
+          p[q] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        o[k] = make_uint4(p[0], p[1], p[2], p[3]);
+      }
+    } else {
+      float4* o = reinterpret_cast<float4*>(out);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o[k] = make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+    }
+  }
+  flags = __syncthreads_or(flags);
+  if (threadIdx.x == 0 && flags) atomicOr(a.status, flags);
+}
+
+// -------------------------------------------------------- host: tensor map
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  // the (rows, 128) bf16 tensor viewed as (2*rows, 64): one 128 B half-row per box row
+  cuuint64_t dims[2] = {64, (cuuint64_t)(2 * nrows)};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, (cuuint32_t)kThreads};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(kv), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int MODE, int G>
+cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
+  auto k = k_enc128<MODE, G>;
+  static std::once_flag once;
+  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); });
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kSmemBytes);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = (a.g.LH * a.g.T + kRows - 1) / kRows;
+  int64_t grid = (int64_t)sm_count * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  k<<<(unsigned)grid, kThreads, kSmemBytes, s>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
+  switch (a.g.group) {
+    case 8: return launch_enc<MODE, 8>(map, a, sm_count, s);
+    case 16: return launch_enc<MODE, 16>(map, a, sm_count, s);
+    case 32: return launch_enc<MODE, 32>(map, a, sm_count, s);
+    case 64: return launch_enc<MODE, 64>(map, a, sm_count, s);
+    default: return launch_enc<MODE, 128>(map, a, sm_count, s);
+  }
+}
+
+template <int MODE, typename Tout, int G>
+cudaError_t launch_dec_g(const DecArgs& a, int sm_count, cudaStream_t s) {
+  auto k = k_dec128<MODE, Tout, G>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.g.LH * a.g.T + kRows - 1) / kRows;
+  int64_t grid = (int64_t)sm_count * per_sm;
+  if (grid > need) grid = need;
+  k<<<(unsigned)grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE, typename Tout>
+cudaError_t launch_dec(const DecArgs& a, int sm_count, cudaStream_t s) {
+  switch (a.g.group) {
+    case 8: return launch_dec_g<MODE, Tout, 8>(a, sm_count, s);
+    case 16: return launch_dec_g<MODE, Tout, 16>(a, sm_count, s);
+    case 32: return launch_dec_g<MODE, Tout, 32>(a, sm_count, s);
+    case 64: return launch_dec_g<MODE, Tout, 64>(a, sm_count, s);
+    default: return launch_dec_g<MODE, Tout, 128>(a, sm_count, s);
+  }
+}
+
+}  // namespace
+
+bool fast128_applicable(const Geo& g) {
+  if (g.C != 128 || g.uchan) return false;
+  if (!(g.group == 8 || g.group == 16 || g.group == 32 || g.group == 64 || g.group == 128)) return false;
+  if (g.transform == T_AFFINE && (g.meta_affine_off % 16) != 0) return false;
+  return true;
+}
+
+cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s) {
+  if (a.g.in_dtype != KVC_DTYPE_BF16) return launch_encode_generic(a, s);
+  const int64_t nrows = a.g.LH * a.g.T;
+  if (2 * nrows >= (1ll << 31)) return launch_encode_generic(a, s);
+  CUtensorMap map;
+  if (!make_input_map(&map, a.kv, nrows)) return launch_encode_generic(a, s);
+  ProfScope ps("encode_fast128", s);
+  switch (a.g.transform) {
+    case T_IDENTITY: return launch_enc_g<M_IDENTITY>(map, a, sm_count, s);
+    case T_DELTA: return launch_enc_g<M_DELTA>(map, a, sm_count, s);
+    case T_HADAMARD: return launch_enc_g<M_HADAMARD>(map, a, sm_count, s);
+    default: return launch_enc_g<M_AFFINE>(map, a, sm_count, s);
+  }
+}
+
+cudaError_t launch_decode_fast128(const DecArgs& a, int sm_count, cudaStream_t s) {
+  if (a.g.transform == T_DELTA) return launch_decode_generic(a, s);
+  ProfScope ps("decode_fast128", s);
+  const bool bf = a.g.out_dtype == KVC_DTYPE_BF16;
+  switch (a.g.transform) {
+    case T_IDENTITY: return bf ? launch_dec<M_IDENTITY, __nv_bfloat16>(a, sm_count, s) : launch_dec<M_IDENTITY, float>(a, sm_count, s);
+    case T_HADAMARD: return bf ? launch_dec<M_HADAMARD, __nv_bfloat16>(a, sm_count, s) : launch_dec<M_HADAMARD, float>(a, sm_count, s);
+    default: return bf ? launch_dec<M_AFFINE, __nv_bfloat16>(a, sm_count, s) : launch_dec<M_AFFINE, float>(a, sm_count, s);
+  }
+}
+
+}  // namespace kvc

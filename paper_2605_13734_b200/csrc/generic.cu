@@ -9,6 +9,8 @@
 
 #include "kernels.h"
 #include "numerics.cuh"
+#include "profile.h"
+#include "rowpos.cuh"
 
 namespace kvc {
 
@@ -111,30 +113,6 @@ __global__ void k_affine_calibrate(Geo g, const Tin* kv, uint8_t* meta) {
     s = fminf(s, 65504.0f);
     mu[lh * g.C + c] = __float2half_rn(m);
     a[lh * g.C + c] = __float2half_rn(s);
-  }
-}
-
-// --------------------------------------------------------- stream positions
-// (width, absolute bit) of quant row (lh, t) in the per-token layout.
-__device__ __forceinline__ void token_row_pos(const Geo& g, const HeadEntry* heads, int64_t lh, int64_t t, int& w,
-                                              int64_t& bit) {
-  if (g.quant == Q_UNIFORM) {
-    w = g.bits;
-    bit = (lh * g.T + t) * g.C * w;
-  } else if (g.quant == Q_MIXTOK) {
-    const int64_t k = g.k_tok, tl = g.T - k;
-    if (t >= tl) {
-      w = g.hi;
-      bit = (lh * k + (t - tl)) * g.C * w;
-    } else {
-      w = g.lo;
-      const int64_t lo_start = ((g.LH * k * g.C * g.hi + 7) / 8) * 8;
-      bit = lo_start + (lh * tl + t) * g.C * w;
-    }
-  } else {
-    HeadEntry e = heads[lh];
-    w = e.w;
-    bit = e.bit + t * g.C * w;
   }
 }
 
@@ -443,6 +421,7 @@ cudaError_t launch_encode_generic(const EncArgs& a, cudaStream_t s) {
   int TT = generic_tile_tokens(g);
   size_t sm = generic_encode_smem(g, TT);
   int64_t tiles = g.LH * ((g.T + TT - 1) / TT);
+  ProfScope ps("encode_generic", s);
   if (g.in_dtype == KVC_DTYPE_BF16) {
     cudaFuncSetAttribute(k_encode_generic<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_encode_generic<__nv_bfloat16><<<(unsigned)tiles, 256, sm, s>>>(a, TT);
@@ -458,6 +437,7 @@ cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s) {
   if (g.transform == T_DELTA) {
     int64_t cols = g.LH * g.C;
     unsigned blocks = (unsigned)((cols + 127) / 128);
+    ProfScope ps("decode_delta", s);
     if (g.out_dtype == KVC_DTYPE_BF16)
       k_decode_delta<__nv_bfloat16><<<blocks, 128, 0, s>>>(a);
     else
@@ -467,6 +447,7 @@ cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s) {
   int TT = generic_tile_tokens(g);
   size_t sm = generic_decode_smem(g, TT);
   int64_t tiles = g.LH * ((g.T + TT - 1) / TT);
+  ProfScope ps("decode_generic", s);
   if (g.out_dtype == KVC_DTYPE_BF16) {
     cudaFuncSetAttribute(k_decode_generic<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_decode_generic<__nv_bfloat16><<<(unsigned)tiles, 256, sm, s>>>(a, TT);
@@ -478,17 +459,20 @@ cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_setup(const Geo& g, const uint8_t* meta, StreamTab* st, HeadEntry* heads, cudaStream_t s) {
+  ProfScope ps("setup", s);
   k_setup<<<1, 32, 0, s>>>(g, meta, st, heads);
   return cudaGetLastError();
 }
 
 cudaError_t launch_write_classmap(const ClassBits& cb, uint8_t* dst, int nbytes, cudaStream_t s) {
+  ProfScope ps("classmap", s);
   k_write_classmap<<<1, 256, 0, s>>>(cb, dst, nbytes);
   return cudaGetLastError();
 }
 
 cudaError_t launch_affine_calibrate(const Geo& g, const void* kv, uint8_t* meta, cudaStream_t s) {
   unsigned thr = (unsigned)(g.C < 256 ? ((g.C + 31) / 32) * 32 : 256);
+  ProfScope ps("affine_calibrate", s);
   if (g.in_dtype == KVC_DTYPE_BF16)
     k_affine_calibrate<__nv_bfloat16><<<(unsigned)g.LH, thr, 0, s>>>(g, reinterpret_cast<const __nv_bfloat16*>(kv), meta);
   else

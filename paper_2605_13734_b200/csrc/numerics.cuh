@@ -115,16 +115,21 @@ __device__ __forceinline__ GroupQ group_setup(float mn, float mx, int w, float r
 }
 
 // rint(fp32((v - z) / s)) clipped to [0, levels] (quantize.py:152-154).
-// Reciprocal + two FMAs reproduce the IEEE quotient (exhaustively checked
-// over all fp16 scales: tools/numerics/markstein_check.c); the pre-clamp at
-// 512 keeps the residual finite; rint is the 1.5*2^23 magic add.
-__device__ __forceinline__ uint32_t quant_fast(float v, const GroupQ& q) {
+// Reciprocal + two FMAs reproduce the IEEE quotient's clipped rint
+// (exhaustively checked over all fp16 scales with |v - z| <= 2^24, which
+// holds whenever scale and zero are finite: tools/numerics/markstein_check.c);
+// rint is the 1.5*2^23 magic add, whose low byte is the symbol.
+__device__ __forceinline__ float quant_magic(float v, const GroupQ& q) {
   float d = __fsub_rn(v, q.z);
-  float q0 = fminf(__fmul_rn(d, q.r), 512.0f);
+  float q0 = __fmul_rn(d, q.r);
   float e = __fmaf_rn(-q0, q.s, d);
   float q1 = __fmaf_rn(e, q.r, q0);
   float c = fminf(fmaxf(q1, 0.0f), q.lv);
-  return __float_as_uint(__fadd_rn(c, kMagicRound)) - kMagicBits;
+  return __fadd_rn(c, kMagicRound);
+}
+
+__device__ __forceinline__ uint32_t quant_fast(float v, const GroupQ& q) {
+  return __float_as_uint(quant_magic(v, q)) - kMagicBits;
 }
 
 __device__ __forceinline__ uint32_t quant_one(float v, const GroupQ& q) {
