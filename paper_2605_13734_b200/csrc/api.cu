@@ -355,6 +355,8 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
   }
   if (fast128_applicable(g))
     e = launch_encode_fast128(a, p.sm_count, s);
+  else if (uchan128_applicable(g))
+    e = launch_encode_uchan128(a, p.sm_count, s);
   else
     e = launch_encode_generic(a, s);
   if (e != cudaSuccess) return cuda_fail(e, "encode kernel");
@@ -424,6 +426,8 @@ static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payloa
   fill_common(p, a.hk, a.hc);
   if (fast128_applicable(g))
     e = launch_decode_fast128(a, p.sm_count, s);
+  else if (uchan128_applicable(g))
+    e = launch_decode_uchan128(a, p.sm_count, s);
   else
     e = launch_decode_generic(a, s);
   if (e != cudaSuccess) return cuda_fail(e, "decode kernel");

@@ -243,7 +243,8 @@ __device__ __forceinline__ void quantize64(float* y, int cb0, int cb1, int w, fl
 }
 
 // ------------------------------------------------------------ encode kernel
-template <int MODE, int G>
+// W = compile-time symbol width (uniform strategies), 0 = per-row runtime width
+template <int MODE, int G, int W>
 __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -358,8 +359,25 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
           f[32 + k] = r - v;
         }
       }
+      // branch-free rounding per 8 values; the rare exact fallback is a cold call
 #pragma unroll
-      for (int i = 0; i < 64; ++i) y[i] = hadamard_out(f[i], a.hk, a.hc, flags);
+      for (int c8 = 0; c8 < 64; c8 += 8) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          bool sl;
+          y[c8 + j] = hadamard_fast(f[c8 + j], a.hk, sl);
+          any |= sl;
+        }
+        if (any) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            bool sl;
+            hadamard_fast(f[c8 + j], a.hk, sl);
+            if (sl) y[c8 + j] = hadamard_slow(f[c8 + j], a.hc, &flags);
+          }
+        }
+      }
       cb0 = 32 * half;
       cb1 = 64 + 32 * half;
       hadlayout = true;
@@ -411,8 +429,13 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     quantize64<G>(y, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros, hadlayout, half, flags);
     if (valid) {
       uint8_t* out = a.packed + (bit >> 3);
-      pack32_dispatch(w, y, out + cb0 * w / 8);
-      pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+      if constexpr (W == 0) {
+        pack32_dispatch(w, y, out + cb0 * w / 8);
+        pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+      } else {
+        pack32_store<W>(y, out + cb0 * W / 8);
+        pack32_store<W>(y + 32, out + cb1 * W / 8);
+      }
     }
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
@@ -438,7 +461,7 @@ __device__ __forceinline__ void dequant64(float* y, int cb0, int cb1, int64_t ro
   }
 }
 
-template <int MODE, typename Tout, int G>
+template <int MODE, typename Tout, int G, int W>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
@@ -461,8 +484,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
     const int cb1 = had ? 64 + 32 * half : 64 * half + 32;
     const uint8_t* src = a.packed + (bit >> 3);
     float y[64];
-    unpack32_dispatch(w, src + cb0 * w / 8, y);
-    unpack32_dispatch(w, src + cb1 * w / 8, y + 32);
+    if constexpr (W == 0) {
+      unpack32_dispatch(w, src + cb0 * w / 8, y);
+      unpack32_dispatch(w, src + cb1 * w / 8, y + 32);
+    } else {
+      unpack32<W>(src + cb0 * W / 8, y);
+      unpack32<W>(src + cb1 * W / 8, y + 32);
+    }
     dequant64<G>(y, cb0, cb1, row, scales, zeros);
     if (MODE == M_HADAMARD) {
       // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
@@ -565,9 +593,9 @@ bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows) {
   return r == CUDA_SUCCESS;
 }
 
-template <int MODE, int G>
+template <int MODE, int G, int W>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
-  auto k = k_enc128<MODE, G>;
+  auto k = k_enc128<MODE, G, W>;
   static std::once_flag once;
   std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); });
   int per_sm = 0;
@@ -580,20 +608,29 @@ cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, c
   return cudaGetLastError();
 }
 
-template <int MODE>
-cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
-  switch (a.g.group) {
-    case 8: return launch_enc<MODE, 8>(map, a, sm_count, s);
-    case 16: return launch_enc<MODE, 16>(map, a, sm_count, s);
-    case 32: return launch_enc<MODE, 32>(map, a, sm_count, s);
-    case 64: return launch_enc<MODE, 64>(map, a, sm_count, s);
-    default: return launch_enc<MODE, 128>(map, a, sm_count, s);
+template <int MODE, int G>
+cudaError_t launch_enc_w(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
+  const int w = a.g.quant == Q_UNIFORM ? a.g.bits : 0;
+  switch (w) {
+    case 2: return launch_enc<MODE, G, 2>(map, a, sm_count, s);
+    case 4: return launch_enc<MODE, G, 4>(map, a, sm_count, s);
+    case 8: return launch_enc<MODE, G, 8>(map, a, sm_count, s);
+    default: return launch_enc<MODE, G, 0>(map, a, sm_count, s);
   }
 }
 
-template <int MODE, typename Tout, int G>
-cudaError_t launch_dec_g(const DecArgs& a, int sm_count, cudaStream_t s) {
-  auto k = k_dec128<MODE, Tout, G>;
+template <int MODE>
+cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
+  switch (a.g.group) {
+    case 32: return launch_enc_w<MODE, 32>(map, a, sm_count, s);
+    case 64: return launch_enc_w<MODE, 64>(map, a, sm_count, s);
+    default: return launch_enc_w<MODE, 128>(map, a, sm_count, s);
+  }
+}
+
+template <int MODE, typename Tout, int G, int W>
+cudaError_t launch_dec_gw(const DecArgs& a, int sm_count, cudaStream_t s) {
+  auto k = k_dec128<MODE, Tout, G, W>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
@@ -604,11 +641,20 @@ cudaError_t launch_dec_g(const DecArgs& a, int sm_count, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int MODE, typename Tout, int G>
+cudaError_t launch_dec_g(const DecArgs& a, int sm_count, cudaStream_t s) {
+  const int w = a.g.quant == Q_UNIFORM ? a.g.bits : 0;
+  switch (w) {
+    case 2: return launch_dec_gw<MODE, Tout, G, 2>(a, sm_count, s);
+    case 4: return launch_dec_gw<MODE, Tout, G, 4>(a, sm_count, s);
+    case 8: return launch_dec_gw<MODE, Tout, G, 8>(a, sm_count, s);
+    default: return launch_dec_gw<MODE, Tout, G, 0>(a, sm_count, s);
+  }
+}
+
 template <int MODE, typename Tout>
 cudaError_t launch_dec(const DecArgs& a, int sm_count, cudaStream_t s) {
   switch (a.g.group) {
-    case 8: return launch_dec_g<MODE, Tout, 8>(a, sm_count, s);
-    case 16: return launch_dec_g<MODE, Tout, 16>(a, sm_count, s);
     case 32: return launch_dec_g<MODE, Tout, 32>(a, sm_count, s);
     case 64: return launch_dec_g<MODE, Tout, 64>(a, sm_count, s);
     default: return launch_dec_g<MODE, Tout, 128>(a, sm_count, s);
@@ -619,7 +665,7 @@ cudaError_t launch_dec(const DecArgs& a, int sm_count, cudaStream_t s) {
 
 bool fast128_applicable(const Geo& g) {
   if (g.C != 128 || g.uchan) return false;
-  if (!(g.group == 8 || g.group == 16 || g.group == 32 || g.group == 64 || g.group == 128)) return false;
+  if (!(g.group == 32 || g.group == 64 || g.group == 128)) return false;
   if (g.transform == T_AFFINE && (g.meta_affine_off % 16) != 0) return false;
   return true;
 }

@@ -75,6 +75,11 @@ bool fast128_applicable(const Geo& g);
 cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_decode_fast128(const DecArgs& a, int sm_count, cudaStream_t s);
 
+// per-channel (q=uchan) head_dim-128 kernels (uchan128.cu)
+bool uchan128_applicable(const Geo& g);
+cudaError_t launch_encode_uchan128(const EncArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_decode_uchan128(const DecArgs& a, int sm_count, cudaStream_t s);
+
 // codec stage (codec.cu)
 size_t codec_scan_bytes(int64_t max_blocks);
 cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s);

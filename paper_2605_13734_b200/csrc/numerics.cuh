@@ -53,21 +53,32 @@ __device__ __forceinline__ double f32bits_scaled_f64(uint32_t f) {
 // hc = c.  Fast path: RN64(S * RN64(1/c)) rounded to f32 with integer ops;
 // exact __ddiv_rn fallback when that product lies within 4 ulp64 of an f32
 // rounding boundary or outside the normal f32 range.
-__device__ __forceinline__ float hadamard_out(double Sp, double hk, double hc, uint32_t& flags) {
-  double q = Sp * hk;
-  uint32_t H = (uint32_t)__double2hiint(q), Lw = (uint32_t)__double2loint(q);
-  uint32_t m = Lw & 0x1FFFFFFFu;
-  uint32_t e = (H >> 20) & 0x7FFu;
-  if ((e - 897u) < 254u && (m - 0x0FFFFFFCu) > 8u) {
-    uint32_t t = __funnelshift_l(Lw, H, 3);
-    t = t - 0xC0000000u + (m > 0x10000000u ? 1u : 0u);
-    return __uint_as_float((t & 0x7FFFFFFFu) | (H & 0x80000000u));
-  }
+// Exact fallback (cold): signed zero, f32 subnormal / overflow range, or a
+// product within 4 ulp64 of an f32 rounding boundary.
+static __device__ __noinline__ float hadamard_slow(double Sp, double hc, uint32_t* flags) {
+  uint32_t H = (uint32_t)__double2hiint(Sp), Lw = (uint32_t)__double2loint(Sp);
   if (((H & 0x7FFFFFFFu) | Lw) == 0u) return __uint_as_float(H & 0x80000000u);  // signed zero
-  double S = Sp * 0x1p896;
-  float y = __double2float_rn(__ddiv_rn(S, hc));
-  if (!isfinite(y)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+  float y = __double2float_rn(__ddiv_rn(Sp * 0x1p896, hc));
+  if (!isfinite(y)) *flags |= KVC_FLAG_NONFINITE_TRANSFORM;
   return y;
+}
+
+// Branch-free fast path: RN64(S * RN64(1/c)) rounded to f32 with integer
+// ops.  `slow` is set when the result must come from hadamard_slow: the
+// magnitude is outside [2^-126, 2^128) or within 4 ulp64 of a midpoint.
+__device__ __forceinline__ float hadamard_fast(double Sp, double hk, bool& slow) {
+  const double q = Sp * hk;
+  const uint32_t H = (uint32_t)__double2hiint(q), Lw = (uint32_t)__double2loint(q);
+  const uint32_t m = Lw & 0x1FFFFFFFu;
+  slow = ((H & 0x7FFFFFFFu) - 0x38100000u >= 0x0FE00000u) | ((m - 0x0FFFFFFCu) <= 8u);
+  const uint32_t t = __funnelshift_l(Lw, H, 3) - 0xC0000000u + (m > 0x10000000u ? 1u : 0u);
+  return __uint_as_float((t & 0x7FFFFFFFu) | (H & 0x80000000u));
+}
+
+__device__ __forceinline__ float hadamard_out(double Sp, double hk, double hc, uint32_t& flags) {
+  bool slow;
+  float y = hadamard_fast(Sp, hk, slow);
+  return slow ? hadamard_slow(Sp, hc, &flags) : y;
 }
 
 // ---------------------------------------------------------------------------
@@ -76,12 +87,16 @@ __device__ __forceinline__ float hadamard_out(double Sp, double hk, double hc, u
 // exactly, so this equals RN16(d/levels); computed in fp32 and checked for
 // proximity to an fp16 boundary (relative 2^-20 vs an error of 2^-23).
 // ---------------------------------------------------------------------------
+static __device__ __noinline__ unsigned short scale16_slow(float d, float levels) {
+  return __half_as_ushort(__double2half(__ddiv_rn((double)d, (double)levels)));
+}
+
 __device__ __forceinline__ __half scale16_exact(float d, float levels, float rl) {
   float q = __fmul_rn(d, rl);
   __half a = __float2half_rn(__fmul_rn(q, 1.00000095367431640625f));
   __half b = __float2half_rn(__fmul_rn(q, 0.99999904632568359375f));
   if (__half_as_ushort(a) == __half_as_ushort(b)) return a;
-  return __double2half(__ddiv_rn((double)d, (double)levels));
+  return __ushort_as_half(scale16_slow(d, levels));
 }
 
 // Per-group quantizer state (quantize.py:146-154).
@@ -132,12 +147,17 @@ __device__ __forceinline__ uint32_t quant_fast(float v, const GroupQ& q) {
   return __float_as_uint(quant_magic(v, q)) - kMagicBits;
 }
 
+// exact slow path (cold): infinite fp16 scale or zero
+static __device__ __noinline__ uint32_t quant_slow(float v, float z, float s, float lv) {
+  float r = rintf(__fdiv_rn(__fsub_rn(v, z), s));
+  r = fminf(fmaxf(r, 0.0f), lv);  // NaN -> 0 like numpy's uint8 cast on x86
+  return (uint32_t)r;
+}
+
 __device__ __forceinline__ uint32_t quant_one(float v, const GroupQ& q) {
   if (q.mode == 0) return quant_fast(v, q);
   if (q.mode == 1) return 0u;
-  float r = rintf(__fdiv_rn(__fsub_rn(v, q.z), q.s));
-  r = fminf(fmaxf(r, 0.0f), q.lv);  // NaN -> 0 like numpy's uint8 cast on x86
-  return (uint32_t)r;
+  return quant_slow(v, q.z, q.s, q.lv);
 }
 
 // dequantize (quantize.py:178): zero + symbol*scale, unfused.

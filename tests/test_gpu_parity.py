@@ -74,7 +74,9 @@ STRATS = [
 def fast_path(sid, shape, in_f32=False):
     s = oracle.parse_id(sid)
     g = s.group
-    return shape[3] == 128 and s.quant != "uchan" and g in (8, 16, 32, 64, 128) and not in_f32
+    if s.quant == "uchan":
+        return shape[3] == 128 and g == 32 and shape[2] % 128 == 0 and not in_f32
+    return shape[3] == 128 and g in (32, 64, 128) and not in_f32
 
 
 def assert_decoded(got, rec, sid, shape, in_f32=False):
@@ -107,6 +109,16 @@ def test_fast128_groups_widths(g, t, b):
     sid = f"t={t};q=uniform,b={b},g={g};c=none"
     shape = (1, 2, 130, 128)
     got, rec, _ = run_case(sid, shape, seed=b * 7 + g)
+    assert_decoded(got, rec, sid, shape)
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("t", ["identity", "affine"])
+@pytest.mark.parametrize("c", ["none", "entropy"])
+def test_uchan128(b, t, c):
+    sid = f"t={t};q=uchan,b={b},g=32;c={c}"
+    shape = (2, 3, 384, 128)
+    got, rec, _ = run_case(sid, shape, seed=b)
     assert_decoded(got, rec, sid, shape)
 
 
