@@ -49,7 +49,7 @@ WORKLOADS = {
                tensors=[("K", "t=affine;q=uniform,b=8,g=32;c=entropy"), ("V", "t=affine;q=uniform,b=8,g=32;c=entropy")],
                shard=False, paged=True),
 }
-BLOCK = 4096
+BLOCK = 2048
 
 
 def _args():
@@ -61,7 +61,12 @@ def _args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    p.add_argument("--block", type=int, default=None, help="codec block symbols (default 2048)")
+    args = p.parse_args()
+    global BLOCK
+    if args.block:
+        BLOCK = args.block
+    return args
 
 
 def _shard_shape(wl, rank, world):

@@ -61,7 +61,7 @@ enum {
 };
 
 typedef struct {
-  int64_t block_symbols; /* codec block (entropy / rle framing); multiple of 8; 0 -> 4096 */
+  int64_t block_symbols; /* codec block (entropy / rle framing); multiple of 8; 0 -> 2048 */
   int32_t in_dtype;      /* KVC_DTYPE_BF16 (serving cache) or KVC_DTYPE_F32 (reference) */
   int32_t out_dtype;     /* decode output dtype                                 */
   int32_t reserved[8];

@@ -96,7 +96,7 @@ class KVCodec:
         shape,
         in_dtype: torch.dtype = torch.bfloat16,
         out_dtype: torch.dtype = torch.bfloat16,
-        block_symbols: int = 4096,
+        block_symbols: int = 2048,
         device: torch.device | str | int | None = None,
     ) -> None:
         L, H, T, C = (int(v) for v in shape)

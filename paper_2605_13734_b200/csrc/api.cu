@@ -215,7 +215,9 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   if ((g.in_dtype != KVC_DTYPE_BF16 && g.in_dtype != KVC_DTYPE_F32) ||
       (g.out_dtype != KVC_DTYPE_BF16 && g.out_dtype != KVC_DTYPE_F32))
     return fail(KVC_ERR_CONFIG, "dtype must be KVC_DTYPE_BF16 or KVC_DTYPE_F32");
-  g.block = (opt && opt->block_symbols) ? opt->block_symbols : 4096;
+  // 2048 symbols: the adaptive model never halves inside a block for
+  // alphabets <= 16 (codecs.py:227-232), which the coder exploits
+  g.block = (opt && opt->block_symbols) ? opt->block_symbols : 2048;
   if (g.block <= 0 || g.block % 8) return fail(KVC_ERR_CONFIG, "block_symbols must be a positive multiple of 8");
   g.uchan = g.quant == Q_UCHAN;
   g.rowlen = g.uchan ? T : C;

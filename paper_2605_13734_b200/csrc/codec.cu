@@ -537,10 +537,8 @@ cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s
   widths_used(a.g, used);
   if (a.g.codec == C_ENTROPY) {
     // one launch per width in use; each thread skips blocks of other widths
-    if (used[1]) launch_rc_encode_w<1>(a, grid, s);
-    if (used[2]) launch_rc_encode_w<2>(a, grid, s);
-    if (used[3]) launch_rc_encode_w<3>(a, grid, s);
-    if (used[4]) launch_rc_encode_w<4>(a, grid, s);
+    for (int w = 1; w <= 4; ++w)
+      if (used[w]) launch_rc_small_encode(a, w, grid, s);
     if (used[5]) launch_rc_encode_w<5>(a, grid, s);
     if (used[6]) launch_rc_encode_w<6>(a, grid, s);
     if (used[7]) launch_rc_encode_w<7>(a, grid, s);
@@ -574,10 +572,8 @@ cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s
   bool used[9];
   widths_used(a.g, used);
   if (a.g.codec == C_ENTROPY) {
-    if (used[1]) launch_rc_decode_w<1>(a, grid, s);
-    if (used[2]) launch_rc_decode_w<2>(a, grid, s);
-    if (used[3]) launch_rc_decode_w<3>(a, grid, s);
-    if (used[4]) launch_rc_decode_w<4>(a, grid, s);
+    for (int w = 1; w <= 4; ++w)
+      if (used[w]) launch_rc_small_decode(a, w, grid, s);
     if (used[5]) launch_rc_decode_w<5>(a, grid, s);
     if (used[6]) launch_rc_decode_w<6>(a, grid, s);
     if (used[7]) launch_rc_decode_w<7>(a, grid, s);

@@ -80,6 +80,11 @@ bool uchan128_applicable(const Geo& g);
 cudaError_t launch_encode_uchan128(const EncArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_decode_uchan128(const DecArgs& a, int sm_count, cudaStream_t s);
 
+// small-alphabet range coder (rc_small.cu), widths 1..4
+bool rc_small_supported(int w);
+cudaError_t launch_rc_small_encode(const CodecArgs& a, int w, unsigned grid, cudaStream_t s);
+cudaError_t launch_rc_small_decode(const CodecArgs& a, int w, unsigned grid, cudaStream_t s);
+
 // codec stage (codec.cu)
 size_t codec_scan_bytes(int64_t max_blocks);
 cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s);

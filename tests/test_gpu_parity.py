@@ -112,6 +112,71 @@ def test_fast128_groups_widths(g, t, b):
     assert_decoded(got, rec, sid, shape)
 
 
+def symbol_stream_kv(pattern, shape, bits, seed):
+    """KV whose identity/uniform quantization yields a chosen symbol stream:
+    every 32-group holds 0 and 2^b-1 (scale 1, zero 0), the other 30 values
+    are the desired symbols."""
+    rng = np.random.default_rng(seed)
+    L, H, T, C = shape
+    lv = (1 << bits) - 1
+    n = L * H * T * C
+    if pattern == "constant":
+        s = np.full(n, 1)
+    elif pattern == "skewed":
+        s = np.minimum(rng.geometric(0.6, n) - 1, lv)
+    elif pattern == "alternating":
+        s = np.arange(n) % (lv + 1)
+    else:
+        s = rng.integers(0, lv + 1, n)
+    s = s.reshape(-1, 32)
+    s[:, 0] = 0
+    s[:, 1] = lv
+    return s.reshape(shape).astype(np.float32)
+
+
+@pytest.mark.parametrize("pattern", ["constant", "skewed", "alternating", "random"])
+@pytest.mark.parametrize("bits", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("block", [256, 2048, 4096, 8192])
+def test_entropy_symbol_streams(pattern, bits, block):
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (1, 2, 72, 128)  # 18432 symbols: tails against every block size
+    v = symbol_stream_kv(pattern, shape, bits, seed=bits * 31 + block)
+    sid = f"t=identity;q=uniform,b={bits},g=32;c=entropy"
+    ref = oracle.encode_blob(v, None, sid, block=block)
+    codec = KVCodec(sid, shape, out_dtype=torch.float32, block_symbols=block)
+    blob = codec.encode(torch.from_numpy(v).to(torch.bfloat16).cuda())
+    codec.check()
+    assert np.array_equal(blob.offsets_array(), ref["offsets"])
+    assert blob.payload_bytes() == ref["payload"]
+    out = codec.decode(blob).cpu().numpy()
+    codec.check(decoding=True)
+    assert np.array_equal(out, v)
+
+
+def test_entropy_decode_rejects_corruption():
+    from paper_2605_13734_b200 import KVCodec, _native
+
+    shape = (1, 2, 64, 128)
+    v = symbol_stream_kv("random", shape, 2, seed=1)
+    sid = "t=identity;q=uniform,b=2,g=32;c=entropy"
+    codec = KVCodec(sid, shape, block_symbols=1024)
+    blob = codec.encode(torch.from_numpy(v).to(torch.bfloat16).cuda())
+    codec.check()
+    n = blob.payload_nbytes()
+    # truncate the first block's coded bytes by lying about its length header
+    blob.payload[0] = blob.payload[0] ^ 0x01
+    codec.decode(blob)
+    with pytest.raises(_native.CodecError):
+        codec.check(decoding=True)
+    blob.payload[0] = blob.payload[0] ^ 0x01
+    # trailing bytes after the last block (codecs.py:429-430)
+    blob._nbytes = n + 3
+    codec.decode(blob)
+    with pytest.raises(_native.CodecError):
+        codec.check(decoding=True)
+
+
 @pytest.mark.parametrize("b", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("t", ["identity", "affine"])
 @pytest.mark.parametrize("c", ["none", "entropy"])
