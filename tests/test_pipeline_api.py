@@ -1,0 +1,141 @@
+"""Reference-facing API on the GPU: compress / decompress / timers /
+evaluator behave like kvpilot.pipeline (tests mirror test_compress.py)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _tensor(shape=(2, 4, 64, 64), seed=0, bf16=False):
+    from paper_2605_13734_b200 import KVTensor
+
+    rng = np.random.default_rng(seed)
+    vals = rng.normal(0, 1.0, shape).astype(np.float32)
+    if bf16:
+        vals = torch.from_numpy(vals).to(torch.bfloat16).float().numpy()
+    return KVTensor(values=vals, head_importance=rng.uniform(0.0, 1.0, shape[:2]))
+
+
+def test_measured_cr_equals_analytic_for_bitpack_codec():  # test_compress.py:18-25
+    from paper_2605_13734_b200 import CostModelTimer, analytic_cr, compress, parse_strategy_id
+
+    t = _tensor()
+    for sid in ("t=identity;q=uniform,b=4,g=32;c=none", "t=identity;q=uniform,b=2,g=32;c=none"):
+        s = parse_strategy_id(sid)
+        blob, m = compress(t, s, timer=CostModelTimer())
+        assert m.cr == pytest.approx(analytic_cr(s), rel=1e-12)
+
+
+def test_fp32_inputs_match_oracle_and_roundtrip():
+    """Arbitrary fp32 (not bf16-exact) inputs take the fp32 plan: blobs equal
+    the oracle's; reconstruction equals the reference's bit for bit."""
+    from paper_2605_13734_b200 import compress, decompress
+
+    t = _tensor(seed=3)
+    for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=delta;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=entropy"):
+        blob, m = compress(t, sid)
+        ref = oracle.encode_blob(t.values, t.head_importance, sid, block=2048)
+        assert blob.payload == ref["payload"] and blob.metadata == ref["metadata"]
+        rec, s_dec = decompress(blob, sid)
+        want = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, t.shape, block=2048)
+        assert np.array_equal(rec.values.cpu().numpy(), want)
+        assert m.quality == pytest.approx(oracle.quality_score(t.values, want), abs=1e-12)
+        assert s_dec > 0 and m.s_enc > 0 and m.s_dec > 0
+
+
+def test_codec_choice_does_not_change_reconstruction():  # test_compress.py:55-64
+    from paper_2605_13734_b200 import compress, decompress
+
+    t = _tensor(seed=4, bf16=True)
+    recs = []
+    for codec in ("none", "rle", "entropy"):
+        sid = f"t=identity;q=uniform,b=4,g=32;c={codec}"
+        blob, _ = compress(t, sid)
+        back, _ = decompress(blob, sid)
+        recs.append(back.values.cpu().numpy())
+    assert np.array_equal(recs[0], recs[1]) and np.array_equal(recs[0], recs[2])
+
+
+def test_host_blob_decodes_without_device_copy():
+    import dataclasses
+
+    from paper_2605_13734_b200 import compress, decompress
+
+    t = _tensor(seed=5, bf16=True)
+    sid = "t=identity;q=uchan,b=2,g=32;c=entropy"
+    blob, _ = compress(t, sid)
+    host_only = dataclasses.replace(blob, device=None)
+    a, _ = decompress(blob, sid)
+    b, _ = decompress(host_only, sid)
+    assert torch.equal(a.values, b.values)
+
+
+def test_decompress_rejects_mismatched_strategy():  # test_compress.py:82-95
+    from paper_2605_13734_b200 import CodecError, compress, decompress
+
+    t = _tensor(seed=7)
+    blob, _ = compress(t, "t=identity;q=uniform,b=4,g=32;c=none")
+    for bad in ("t=identity;q=uniform,b=4,g=16;c=none", "t=identity;q=uniform,b=3,g=32;c=none",
+                "t=identity;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=none"):
+        with pytest.raises(CodecError):
+            decompress(blob, bad)
+
+
+def test_nonfinite_input_raises_value_error():  # tensors.py:41-42
+    from paper_2605_13734_b200 import KVTensor, compress
+
+    v = torch.randn(1, 2, 8, 128, device="cuda", dtype=torch.bfloat16)
+    v[0, 1, 3, 7] = float("nan")
+    with pytest.raises(ValueError):
+        compress(KVTensor(v), "t=identity;q=uniform,b=4,g=32;c=none")
+    with pytest.raises(ValueError):
+        KVTensor(np.full((1, 1, 2, 4), np.inf, np.float32))
+
+
+def test_quality_improves_with_bits():  # test_compress.py:73-79
+    from paper_2605_13734_b200 import CostModelTimer, compress
+
+    t = _tensor(seed=6)
+    q = [compress(t, f"t=identity;q=uniform,b={b},g=32;c=none", timer=CostModelTimer())[1].quality for b in (2, 4, 8)]
+    assert q[0] < q[1] < q[2]
+
+
+def test_cuda_event_timer_and_evaluator():
+    from paper_2605_13734_b200 import CudaEventTimer, GpuCorpusEvaluator, KVTensor, parse_strategy_id
+
+    corpus = []
+    for i in range(6):
+        v, imp = oracle.generate_kv(2, 4, 256, 128, seed=i)
+        corpus.append(KVTensor(torch.from_numpy(v).to(torch.bfloat16).cuda(), imp))
+    ev = GpuCorpusEvaluator(corpus, sample_size=3, timer=CudaEventTimer(repeats=2))
+    s = parse_strategy_id("t=hadamard;q=uniform,b=4,g=32;c=none")
+    acc, cr, lat = ev(s)
+    assert 0.8 < acc < 1.0 and cr == pytest.approx(3.2) and lat > 0
+    s_enc, s_dec = ev.throughputs[s.id]
+    assert s_enc > 1e9 and s_dec > 1e9  # GB/s-scale on the GPU
+    assert ev(s)[:2] == (acc, cr)  # sampling is a function of (seed, id)
+
+
+def test_paged_decode_matches_contiguous():
+    from paper_2605_13734_b200 import KVCodec
+
+    L, H, T, C = 2, 4, 256, 128
+    v, _ = oracle.generate_kv(L, H, T, C, seed=9)
+    kv = torch.from_numpy(v).to(torch.bfloat16).cuda()
+    for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=identity;q=uchan,b=2,g=32;c=entropy",
+                "t=affine;q=uniform,b=8,g=32;c=entropy", "t=delta;q=uniform,b=8,g=32;c=none"):
+        codec = KVCodec(sid, (L, H, T, C))
+        blob = codec.encode(kv)
+        flat = codec.decode(blob)
+        P = 16
+        npages = T // P + 3
+        table = torch.randperm(npages, device="cuda")[: T // P].to(torch.int32)
+        pages = torch.zeros(L * npages * P * H * C, dtype=torch.bfloat16, device="cuda")
+        codec.decode_paged(blob, pages, table, P, npages * P * H * C)
+        codec.check(decoding=True)
+        pv = pages.view(L, npages, P, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
+        assert torch.equal(pv, flat), sid
