@@ -62,6 +62,7 @@ def _args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--block", type=int, default=None, help="codec block symbols (default 2048)")
+    p.add_argument("--streams", type=int, default=1, help="1: one CUDA stream per KV tensor (default); 0: serial")
     args = p.parse_args()
     global BLOCK
     if args.block:
@@ -206,9 +207,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = len(os.sched_getaffinity(0))
-        gbs, nb, wall, tok = cpu_roundtrip(wl, procs, procs)
+        gbs, nb, wall, tok = cpu_roundtrip(wl, 4 * procs, procs)
         cpu = {"value": round(gbs, 6), "unit": "GB/s", "cores": procs, "kind": "port",
-               "sample": f"{procs} head slabs x {tok} tokens x {wl['shape'][3]} ch of this workload's strategies, "
+               "sample": f"{4 * procs} head slabs x {tok} tokens x {wl['shape'][3]} ch of this workload's strategies, "
                          f"oracle round trip on {procs} processes ({wall:.1f} s wall)"}
 
     import numpy as np
@@ -232,8 +233,13 @@ def main():
         kv, imp = synthetic_kv(L, H, T, C, seed=1000 * rank + 17 * ti + l0, device=dev)
         codec = KVCodec(sid, shape, block_symbols=BLOCK, device=dev)
         blob = codec.alloc_blob()
-        out = torch.empty_like(kv)
+        # a 70B 128K cache on one GPU: K, V (2 x 39 GiB) + payloads leave room
+        # for one decode target only -> the tensors share it (serial streams)
+        share = wl["shard"] and world == 1
+        out = tensors[0]["out"] if (share and tensors) else torch.empty_like(kv)
         tensors.append(dict(name=name, sid=sid, kv=kv, codec=codec, blob=blob, out=out))
+    if wl["shard"] and world == 1:
+        args.streams = 0
     torch.cuda.synchronize()
     V_rank = 2 * E * len(tensors)  # bf16-in bytes per step on this rank
 
@@ -246,16 +252,39 @@ def main():
         for t in tensors:
             t["out"] = torch.empty(L * n_pages * page_tokens * H * C, dtype=torch.bfloat16, device=dev)
 
-    def encode_all():
+    # K and V are independent: each runs on its own stream so the HBM-bound
+    # quantize kernels of one overlap the issue-bound range coder of the other
+    main = torch.cuda.current_stream()
+    for t in tensors:
+        t["stream"] = torch.cuda.Stream(device=dev) if args.streams else main
+
+    def _fork():
+        e = torch.cuda.Event()
+        e.record(main)
         for t in tensors:
-            t["codec"].encode(t["kv"], out=t["blob"])
+            t["stream"].wait_event(e)
+
+    def _join():
+        for t in tensors:
+            e = torch.cuda.Event()
+            e.record(t["stream"])
+            main.wait_event(e)
+
+    def encode_all():
+        _fork()
+        for t in tensors:
+            t["codec"].encode(t["kv"], out=t["blob"], stream=t["stream"])
+        _join()
 
     def decode_all():
+        _fork()
         for t in tensors:
             if paged:
-                t["codec"].decode_paged(t["blob"], t["out"], paged["table"], paged["page_tokens"], paged["layer_stride"])
+                t["codec"].decode_paged(t["blob"], t["out"], paged["table"], paged["page_tokens"], paged["layer_stride"],
+                                        stream=t["stream"])
             else:
-                t["codec"].decode(t["blob"], out=t["out"], device_length=True)
+                t["codec"].decode(t["blob"], out=t["out"], device_length=True, stream=t["stream"])
+        _join()
 
     for _ in range(args.warmup):
         encode_all()
@@ -311,14 +340,21 @@ def main():
     # quality of the round trip (reference quality_score, tensors.py:115-134)
     qual = []
     for t in tensors:
-        if paged:
-            pg = t["out"].view(L, -1, paged["page_tokens"], H, C)[:, paged["table"].long()]
-            rec = pg.reshape(L, T, H, C).permute(0, 2, 1, 3).float()
-        else:
-            rec = t["out"].float()
-        x = t["kv"].float()
-        rmse = torch.sqrt(torch.mean((x - rec) ** 2)).item()
-        rms = torch.sqrt(torch.mean(x * x)).item()
+        if t["out"] is tensors[0]["out"] and t is not tensors[0]:
+            t["codec"].decode(t["blob"], out=t["out"], device_length=True)  # shared decode target
+        elif t is tensors[0] and len(tensors) > 1 and tensors[1]["out"] is t["out"]:
+            t["codec"].decode(t["blob"], out=t["out"], device_length=True)
+        se = sx = 0.0
+        for li in range(L):  # per layer: no full-size fp32 temporaries
+            if paged:
+                pg = t["out"].view(L, -1, paged["page_tokens"], H, C)[li, paged["table"].long()]
+                rec = pg.reshape(T, H, C).permute(1, 0, 2).double()
+            else:
+                rec = t["out"][li].double()
+            x = t["kv"][li].double()
+            se += float(((x - rec) ** 2).sum())
+            sx += float((x * x).sum())
+        rmse, rms = math.sqrt(se / E), math.sqrt(sx / E)
         qual.append(max(0.0, 1.0 - rmse / rms) if rmse > 1e-9 else 1.0)
 
     step_ms = total_ms / args.steps
@@ -329,10 +365,15 @@ def main():
     # ---------------- per-kernel times (dominant kernel roofline)
     N.profile_enable(True)
     prof_steps = 2
+    saved = [t["stream"] for t in tensors]
+    for t in tensors:  # per-kernel event times are only meaningful serialised
+        t["stream"] = main
     for _ in range(prof_steps):
         encode_all()
         decode_all()
     prof = N.profile_collect()
+    for t, s_ in zip(tensors, saved):
+        t["stream"] = s_
     N.profile_enable(False)
     launches_per_step = sum(c for _, c in prof.values()) / prof_steps
     peaks = {}

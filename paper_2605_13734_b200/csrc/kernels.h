@@ -85,6 +85,10 @@ bool rc_small_supported(int w);
 cudaError_t launch_rc_small_encode(const CodecArgs& a, int w, unsigned grid, cudaStream_t s);
 cudaError_t launch_rc_small_decode(const CodecArgs& a, int w, unsigned grid, cudaStream_t s);
 
+// large-alphabet range coder (rc_large.cu), widths 5..8
+cudaError_t launch_rc_large_encode(const CodecArgs& a, int w, cudaStream_t s);
+cudaError_t launch_rc_large_decode(const CodecArgs& a, int w, cudaStream_t s);
+
 // codec stage (codec.cu)
 size_t codec_scan_bytes(int64_t max_blocks);
 cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s);
