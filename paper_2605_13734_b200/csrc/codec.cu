@@ -14,6 +14,7 @@
 
 #include "kernels.h"
 #include "profile.h"
+#include "rc_tables.cuh"
 
 namespace kvc {
 
@@ -172,8 +173,10 @@ size_t codec_scan_bytes(int64_t max_blocks) {
   return bytes + 256;
 }
 
-cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s) {
+cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_t s) {
   (void)sm_count;
+  CodecArgs a = args;
+  if (a.g.codec == C_ENTROPY) a.recip = recip_tables(s);
   const unsigned grid = (unsigned)((a.max_blocks + 1 + 127) / 128);
   bool used[9];
   widths_used(a.g, used);
@@ -202,8 +205,10 @@ cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s) {
+cudaError_t launch_codec_decode(const CodecArgs& args, int sm_count, cudaStream_t s) {
   (void)sm_count;
+  CodecArgs a = args;
+  if (a.g.codec == C_ENTROPY) a.recip = recip_tables(s);
   {
     ProfScope ps("check_payload", s);
     k_check_payload<<<1, 1, 0, s>>>(a);

@@ -55,6 +55,7 @@ struct CodecArgs {
   int64_t max_blocks;
   int64_t payload_bytes;      // decode: caller's payload length
   uint32_t* status;
+  const uint32_t* recip;      // [9][2048] reciprocal tables (rc_tables.cuh)
 };
 
 __device__ __forceinline__ int64_t out_index(const DecArgs& a, int64_t lh, int64_t t, int64_t c) {

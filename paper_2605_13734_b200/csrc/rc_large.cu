@@ -2,113 +2,111 @@
 // c=entropy path of the 8-bit profiles (BASELINE config 5).
 //
 // Bit-exact with codecs.py:181-331 per block; one thread per block.  The
-// order-0 model (codecs.py:188-242) is a Fenwick tree of u16 counts plus the
-// u16 frequencies, in shared memory, element j of thread t at [j][t] so a
-// warp's accesses to the same element are conflict-free.  Prefix and update
-// paths are known from the symbol up front, so their loads issue together
-// instead of as a dependent chain.  Before the first halving (symbol
-// H = ceil((65536 - A) / 32)) the total is A + 32 i for every lane and
-// `range // total` uses a per-position reciprocal table (as in rc_small.cu).
+// order-0 model (codecs.py:188-242) is ONE u16 Fenwick tree of frequencies
+// per thread in shared memory (512 B at A = 256), element j of thread t at
+// [j][t] so a warp's accesses to the same node are conflict-free; a symbol's
+// frequency is a Fenwick point query, so no separate frequency array is kept
+// and twice as many blocks fit per SM.  Prefix / point / update paths are
+// known from the symbol up front, so their shared loads issue together.
+// Node values never exceed the running total (< 2^16): a bump that would
+// reach 2^16 takes the halving path (frequencies recovered from the tree,
+// incremented, halved, tree rebuilt) before any node is written.  Before the
+// first halving `range // total` uses the reciprocal table (rc_tables.cuh).
 #include <cstdint>
-#include <type_traits>
 
 #include "kernels.h"
 #include "profile.h"
+#include "rc_tables.cuh"
 
 namespace kvc {
 namespace {
 
 constexpr uint32_t kTop = 1u << 24;
 constexpr uint32_t kBot = 1u << 16;
-constexpr int kLThreads = 64;
-constexpr int kMaxHL = 2048;
+constexpr int kLThreads = 128;
 
 template <int W>
 __host__ __device__ constexpr int halving_at() {
   return (65536 - (1 << W) + 31) / 32;
 }
 
-__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t d, uint32_t m) {
-  const uint32_t q = __umulhi(n, m);
-  return q + ((n - q * d) >= d ? 1u : 0u);
-}
-
-// Frequencies fit u16 for A >= 64 (f + 32 <= 65535 - (A-1) + 32); A = 32 can
-// reach 65536 in long blocks, so small alphabets keep u32 (smem is cheap there).
-// Tree nodes are only read while total < 2^16, so u16 suffices.
-template <int W>
-using FreqT = typename std::conditional<(W <= 6), uint32_t, uint16_t>::type;
-
 template <int W>
 struct LModel {
   static constexpr int A = 1 << W;
-  static constexpr int LOG = W;
-  FreqT<W>* f;     // f[j * kLThreads]
-  FreqT<W>* tree;  // tree[(j-1) * kLThreads], j = 1..A
+  uint16_t* tree;  // node j (1..A) at tree[(j - 1) * kLThreads]
   uint32_t total;
-  __device__ __forceinline__ uint32_t F(int j) const { return f[j * kLThreads]; }
-  __device__ __forceinline__ uint32_t T(int j) const { return tree[(j - 1) * kLThreads]; }
-  __device__ void rebuild() {
-    for (int j = 1; j <= A; ++j) tree[(j - 1) * kLThreads] = 0;
-    for (int j = 1; j <= A; ++j) {
-      const uint32_t v = T(j) + F(j - 1);
-      tree[(j - 1) * kLThreads] = (FreqT<W>)v;
-      const int p = j + (j & -j);
-      if (p <= A) tree[(p - 1) * kLThreads] = (FreqT<W>)(T(p) + v);
-    }
-  }
-  __device__ void init(FreqT<W>* base, int lane) {
-    f = base + lane;
-    tree = base + A * kLThreads + lane;
-    for (int j = 0; j < A; ++j) f[j * kLThreads] = 1;
+  __device__ __forceinline__ uint32_t T(uint32_t j) const { return tree[(j - 1) * kLThreads]; }
+  __device__ __forceinline__ void set(uint32_t j, uint32_t v) { tree[(j - 1) * kLThreads] = (uint16_t)v; }
+  __device__ void init(uint16_t* base, int lane) {
+    tree = base + lane;
+    for (uint32_t j = 1; j <= (uint32_t)A; ++j) set(j, j & (0u - j));  // all frequencies 1
     total = A;
-    rebuild();
   }
-  // sum of f[0..s-1]: the log2(A)+1 nodes of the path are independent loads
+  // sum of f[0..s-1]
   __device__ __forceinline__ uint32_t prefix(uint32_t s) const {
-    uint32_t c = 0;
-    uint32_t i = s;
+    uint32_t c = 0, i = s;
 #pragma unroll
-    for (int k = 0; k <= LOG; ++k) {
-      const uint32_t v = i ? T((int)i) : 0u;
-      c += v;
-      i &= i - 1;  // clear the lowest set bit
+    for (int k = 0; k < W; ++k) {
+      c += i ? T(i) : 0u;
+      i &= i - 1;
     }
     return c;
   }
-  __device__ __forceinline__ void bump(uint32_t s) {
-    f[s * kLThreads] = (FreqT<W>)(F((int)s) + 32u);
-    uint32_t i = s + 1;
+  // f[s] = T(s+1) - sum of the nodes between (s+1) - lowbit(s+1) and s
+  __device__ __forceinline__ uint32_t freq(uint32_t s) const {
+    const uint32_t i = s + 1;
+    const uint32_t stop = i - (i & (0u - i));
+    uint32_t v = T(i), j = s;
 #pragma unroll
-    for (int k = 0; k <= LOG; ++k) {
-      if (i <= (uint32_t)A) tree[(i - 1) * kLThreads] = (FreqT<W>)(T((int)i) + 32u);
-      i += i & (0u - i);
+    for (int k = 0; k < W; ++k) {
+      v -= (j > stop) ? T(j) : 0u;
+      j = (j > stop) ? (j & (j - 1)) : j;
     }
-    total += 32;
+    return v;
   }
-  __device__ void halve() {  // codecs.py:234-242
+  // codecs.py:227-242: f[s] += 32, total += 32, halve at 2^16
+  __device__ __forceinline__ void bump(uint32_t s) {
+    if (total + 32u < 65536u) {
+      uint32_t i = s + 1;
+#pragma unroll
+      for (int k = 0; k <= W; ++k) {
+        if (i <= (uint32_t)A) set(i, T(i) + 32u);
+        i += i & (0u - i);
+      }
+      total += 32u;
+    } else {
+      halve_with(s);
+    }
+  }
+  __device__ void halve_with(uint32_t s) {
+    // tree -> frequencies in place (inverse build), bump s, halve, rebuild
+    for (uint32_t j = A; j >= 1; --j) {
+      const uint32_t p = j + (j & (0u - j));
+      if (p <= (uint32_t)A) set(p, T(p) - T(j));
+    }
+    const uint32_t fs = T(s + 1) + 32u;  // may be 2^16 for A = 32: kept in 32 bits
     uint32_t t = 0;
-    for (int j = 0; j < A; ++j) {
-      uint32_t h = F(j) >> 1;
+    for (uint32_t j = 1; j <= (uint32_t)A; ++j) {
+      uint32_t h = (j == s + 1 ? fs : T(j)) >> 1;
       h = h ? h : 1u;
-      f[j * kLThreads] = (FreqT<W>)h;
+      set(j, h);
       t += h;
     }
     total = t;
-    rebuild();
+    for (uint32_t j = 1; j <= (uint32_t)A; ++j) {
+      const uint32_t p = j + (j & (0u - j));
+      if (p <= (uint32_t)A) set(p, T(p) + T(j));
+    }
   }
   // largest s with prefix(s) <= target (codecs.py:214-225); cum = prefix(s)
   __device__ __forceinline__ uint32_t find(uint32_t target, uint32_t& cum) const {
     uint32_t pos = 0, rem = target;
 #pragma unroll
-    for (int bit = A; bit; bit >>= 1) {
-      const uint32_t nx = pos + bit;
-      if (nx <= (uint32_t)A) {
-        const uint32_t v = T((int)nx);
-        if (v <= rem) {
-          rem -= v;
-          pos = nx;
-        }
+    for (uint32_t bit = A / 2; bit; bit >>= 1) {  // node A holds the total > target
+      const uint32_t v = T(pos + bit);
+      if (v <= rem) {
+        rem -= v;
+        pos += bit;
       }
     }
     cum = target - rem;
@@ -120,11 +118,8 @@ template <int W>
 __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
   constexpr int A = 1 << W;
   constexpr int H = halving_at<W>();
-  extern __shared__ __align__(16) unsigned char lsm_raw[];
-  FreqT<W>* lsm = reinterpret_cast<FreqT<W>*>(lsm_raw);
-  uint32_t* magic = reinterpret_cast<uint32_t*>(lsm + 2 * A * kLThreads);
-  for (int i = threadIdx.x; i < H; i += blockDim.x) magic[i] = (uint32_t)(0x100000000ull / (uint64_t)(A + 32 * i));
-  __syncthreads();
+  extern __shared__ __align__(16) uint16_t lsm[];
+  const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b > a.max_blocks) return;
   const StreamTab st = *a.st;
@@ -146,14 +141,14 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
   int nb = 0, pos = 0;
   for (int i = 0; i < n; ++i) {
     if (nb < W) {
-      buf = (buf << 8) | src[pos++];
+      buf = (buf << 8) | __ldg(src + pos++);
       nb += 8;
     }
     nb -= W;
     const uint32_t s = (buf >> nb) & (A - 1);
     const uint32_t cum = m.prefix(s);
-    const uint32_t fr = m.F((int)s);
-    const uint32_t unit = (i < H) ? div_magic(range, m.total, magic[i]) : range / m.total;
+    const uint32_t fr = m.freq(s);
+    const uint32_t unit = (i < H) ? div_recip(range, m.total, __ldg(magic + i)) : range / m.total;
     low += unit * cum;
     range = unit * fr;
     for (;;) {
@@ -168,7 +163,6 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
       range <<= 8;
     }
     m.bump(s);
-    if (m.total >= 65536u) m.halve();
   }
   for (int k = 0; k < 4; ++k) {
     acc = __funnelshift_l(low, acc, 8);
@@ -184,11 +178,8 @@ template <int W>
 __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   constexpr int A = 1 << W;
   constexpr int H = halving_at<W>();
-  extern __shared__ __align__(16) unsigned char lsm_raw[];
-  FreqT<W>* lsm = reinterpret_cast<FreqT<W>*>(lsm_raw);
-  uint32_t* magic = reinterpret_cast<uint32_t*>(lsm + 2 * A * kLThreads);
-  for (int i = threadIdx.x; i < H; i += blockDim.x) magic[i] = (uint32_t)(0x100000000ull / (uint64_t)(A + 32 * i));
-  __syncthreads();
+  extern __shared__ __align__(16) uint16_t lsm[];
+  const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const StreamTab st = *a.st;
   if (b >= st.nblocks) return;
@@ -219,7 +210,7 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   uint64_t acc = 0;
   int nacc = 0, nout = 0;
   for (int i = 0; i < n; ++i) {
-    const uint32_t unit = (i < H) ? div_magic(range, m.total, magic[i]) : range / m.total;
+    const uint32_t unit = (i < H) ? div_recip(range, m.total, __ldg(magic + i)) : range / m.total;
     uint32_t s, cum;
     if (code >= low) {
       uint32_t target = (code - low) / unit;
@@ -229,7 +220,7 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
       s = 0;
       cum = 0;
     }
-    const uint32_t fr = m.F((int)s);
+    const uint32_t fr = m.freq(s);
     low += unit * cum;
     range = unit * fr;
     for (;;) {
@@ -247,7 +238,6 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
       range <<= 8;
     }
     m.bump(s);
-    if (m.total >= 65536u) m.halve();
     acc = (acc << W) | s;
     nacc += W;
     if (nacc >= 8) {
@@ -260,7 +250,7 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
 
 template <int W>
 size_t large_smem() {
-  return (size_t)2 * (1 << W) * kLThreads * sizeof(FreqT<W>) + (size_t)halving_at<W>() * 4;
+  return (size_t)(1 << W) * kLThreads * sizeof(uint16_t);
 }
 
 template <int W>

@@ -7,7 +7,8 @@
 // is exactly A + 32 i for every lane (codecs.py:227-232: no halving can
 // happen before it), so
 //   * `range // total` is a multiply by a per-position reciprocal from a
-//     shared-memory table plus one correction (div_magic), and
+//     global read-only table (rc_tables.cuh, warp-uniform index) plus one
+//     correction (div_magic), and
 //   * no halving check is needed inside that loop.
 // The remainder of a longer block (after the first halving) and short tails
 // run a generic per-symbol loop with hardware division.  Cumulative
@@ -17,6 +18,7 @@
 
 #include "kernels.h"
 #include "profile.h"
+#include "rc_tables.cuh"
 
 namespace kvc {
 namespace {
@@ -186,9 +188,7 @@ struct Grp {
 template <int W>
 __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
   constexpr int A = 1 << W;
-  __shared__ uint32_t magic[kH];
-  for (int i = threadIdx.x; i < kH; i += blockDim.x) magic[i] = (uint32_t)(0x100000000ull / (uint64_t)(A + 32 * i));
-  __syncthreads();
+  const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b > a.max_blocks) return;
   const StreamTab st = *a.st;
@@ -313,9 +313,7 @@ __device__ __forceinline__ uint32_t dec_symbol(Dec& d, SModel<W>& m, uint32_t un
 template <int W>
 __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   constexpr int A = 1 << W;
-  __shared__ uint32_t magic[kH];
-  for (int i = threadIdx.x; i < kH; i += blockDim.x) magic[i] = (uint32_t)(0x100000000ull / (uint64_t)(A + 32 * i));
-  __syncthreads();
+  const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const StreamTab st = *a.st;
   if (b >= st.nblocks) return;

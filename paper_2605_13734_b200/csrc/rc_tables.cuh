@@ -1,0 +1,26 @@
+// Per-position reciprocal tables for the range coders.
+//
+// Before the first model halving the total at symbol i is A + 32 i
+// (codecs.py:227-232), identical for every block; recip(A)[i] =
+// floor(2^32 / (A + 32 i)) turns `range // total` into a multiply plus one
+// correction.  One table per alphabet size (A = 2..256), built once per
+// device, read through the read-only path with a warp-uniform index.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kvc {
+
+constexpr int kRecipLen = 2048;  // >= ceil((65536 - A) / 32) for every A >= 2
+
+// device pointer to the [9][kRecipLen] table (row w = alphabet 2^w); builds
+// it on first use for the current device (stream-ordered on `s`)
+const uint32_t* recip_tables(cudaStream_t s);
+
+__device__ __forceinline__ uint32_t div_recip(uint32_t n, uint32_t d, uint32_t m) {
+  // floor(n / d) given m = floor(2^32 / d): the product estimate is q or q-1
+  const uint32_t q = __umulhi(n, m);
+  return q + ((n - q * d) >= d ? 1u : 0u);
+}
+
+}  // namespace kvc
