@@ -223,6 +223,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # keep stdout to the one JSON line (NCCL prints a version banner at VERSION level)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
     shape, (l0, l1) = _shard_shape(wl, rank, world)
     L, H, T, C = shape

@@ -132,16 +132,32 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
 }
 
 // ---------------------------------------------------------- scan + gather
-// one warp per block copies its slot bytes to payload[offsets[b]]
+// one warp per block copies its slot bytes to payload[offsets[b]]: partial
+// head / tail words byte by byte (they are shared with the neighbouring
+// blocks), the aligned body as 32-bit words funnel-shifted out of the
+// 16-byte-aligned slot
 __global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const StreamTab& st = *a.st;
   if (b >= st.nblocks) return;
   const uint64_t o0 = a.offsets[b], o1 = a.offsets[b + 1];
+  const uint32_t len = (uint32_t)(o1 - o0);
   const uint8_t* src = a.slots + b * a.slot_bytes;
   uint8_t* dst = a.payload_out + o0;
-  for (uint64_t k = lane; k < o1 - o0; k += 32) dst[k] = src[k];
+  const uint32_t head = min((uint32_t)((4u - (uint32_t)(o0 & 3u)) & 3u), len);
+  const uint32_t words = (len - head) >> 2;
+  const uint32_t tail = len - head - 4 * words;
+  if (lane < (int)head) dst[lane] = src[lane];
+  if (lane < (int)tail) dst[head + 4 * words + lane] = src[head + 4 * words + lane];
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+  const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
+  for (uint32_t w = lane; w < words; w += 32) {
+    const uint32_t lo = s32[w];
+    const uint32_t v = sh ? __funnelshift_r(lo, s32[w + 1], sh) : lo;
+    d32[w] = v;
+  }
 }
 
 // decode-side checks: offsets[0] == 0, offsets[nblocks] == payload bytes

@@ -7,13 +7,15 @@
 // is exactly A + 32 i for every lane (codecs.py:227-232: no halving can
 // happen before it), so
 //   * `range // total` is a multiply by a per-position reciprocal from a
-//     global read-only table (rc_tables.cuh, warp-uniform index) plus one
-//     correction (div_magic), and
+//     global read-only table (rc_tables.cuh; each 32-symbol group's entries
+//     are prefetched into registers) plus one correction, and
 //   * no halving check is needed inside that loop.
 // The remainder of a longer block (after the first halving) and short tails
 // run a generic per-symbol loop with hardware division.  Cumulative
-// frequencies live in registers (16-bit fields of one 64-bit word for
-// A <= 4); bytes are emitted / pulled with one funnel shift each.
+// frequencies C[1..A-1] live in registers; lookup and update share the
+// predicates (s >= k); the decoder's symbol search for A <= 4 is branch-free
+// (compare x = code - low against unit * C[k]).  Bytes are emitted / pulled
+// with one funnel shift each.
 #include <cstdint>
 
 #include "kernels.h"
@@ -27,97 +29,32 @@ constexpr uint32_t kTop = 1u << 24;
 constexpr uint32_t kBot = 1u << 16;
 constexpr int kH = 2048;  // first halving after symbol kH-1 for every A in 2..16
 
-__device__ __forceinline__ uint32_t div_magic(uint32_t n, uint32_t d, uint32_t m) {
-  // floor(n / d) with m = floor(2^32 / d): the estimate is q or q-1
-  const uint32_t q = __umulhi(n, m);
-  return q + ((n - q * d) >= d ? 1u : 0u);
-}
-
-// ----------------------------------------------------------------- models
-template <int W, bool kPacked = (W <= 2)>
-struct SModel;
-
 template <int W>
-struct SModel<W, true> {  // A <= 4: fields [0 | C1 | C2 | C3] of a 64-bit word
+struct SModel {
   static constexpr int A = 1 << W;
-  uint64_t M;
+  uint32_t C[A];  // C[k] = sum of f[0..k-1] for k = 1..A-1 (C[0] unused)
   uint32_t total;
-  __device__ void init() {
-    M = 0;
+  __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int k = 1; k < A; ++k) M |= (uint64_t)k << (16 * k);
-    total = A;
-  }
-  __device__ __forceinline__ uint32_t field(int k) const { return (uint32_t)(M >> (16 * k)) & 0xFFFFu; }
-  __device__ __forceinline__ void lookup(uint32_t s, uint32_t& lo, uint32_t& hi) const {
-    lo = (uint32_t)(M >> (16 * s)) & 0xFFFFu;
-    hi = (s == A - 1) ? total : (uint32_t)(M >> (16 * (s + 1))) & 0xFFFFu;
-  }
-  __device__ __forceinline__ void add(uint32_t s) {
-    constexpr uint64_t inc = (A == 4) ? ((32ull << 16) | (32ull << 32) | (32ull << 48)) : (32ull << 16);
-    M += inc << (16 * s);
-  }
-  __device__ void halve() {
-    uint32_t prev = 0, t = 0;
-    uint64_t nm = 0;
-#pragma unroll
-    for (int k = 1; k <= A; ++k) {
-      const uint32_t ck = (k == A) ? total : field(k);
-      uint32_t f = (ck - prev) >> 1;
-      f = f ? f : 1u;
-      prev = ck;
-      t += f;
-      if (k < A) nm |= (uint64_t)t << (16 * k);
-    }
-    M = nm;
-    total = t;
-  }
-  // decode: largest s with C[s]*unit <= x; returns the scaled bounds
-  __device__ __forceinline__ uint32_t find(uint32_t x, uint32_t unit, uint32_t& plo, uint32_t& phi) const {
-    uint32_t p[A + 1];
-    p[0] = 0;
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 1; k < A; ++k) {
-      p[k] = unit * field(k);
-      s += (x >= p[k]) ? 1u : 0u;
-    }
-    p[A] = unit * total;
-    plo = 0;
-    phi = p[1];
-#pragma unroll
-    for (int k = 1; k < A; ++k) {
-      plo = (s == (uint32_t)k) ? p[k] : plo;
-      phi = (s == (uint32_t)k) ? p[k + 1] : phi;
-    }
-    return s;
-  }
-};
-
-template <int W>
-struct SModel<W, false> {  // A = 8, 16: cumulative counts in registers
-  static constexpr int A = 1 << W;
-  uint32_t C[A];
-  uint32_t total;
-  __device__ void init() {
-#pragma unroll
-    for (int k = 0; k < A; ++k) C[k] = k;
+    for (int k = 1; k < A; ++k) C[k] = k;
     total = A;
   }
   __device__ __forceinline__ void lookup(uint32_t s, uint32_t& lo, uint32_t& hi) const {
     lo = 0;
-    hi = total;
+    hi = C[1];
 #pragma unroll
     for (int k = 1; k < A; ++k) {
-      lo = (s == (uint32_t)k) ? C[k] : lo;
-      hi = (s + 1 == (uint32_t)k) ? C[k] : hi;
+      const bool ge = s >= (uint32_t)k;
+      lo = ge ? C[k] : lo;
+      hi = ge ? (k + 1 < A ? C[k + 1] : total) : hi;
     }
   }
-  __device__ __forceinline__ void add(uint32_t s) {
+  __device__ __forceinline__ void add(uint32_t s) {  // f[s] += 32 (codecs.py:227-230)
 #pragma unroll
-    for (int k = 1; k < A; ++k) C[k] += ((uint32_t)k > s) ? 32u : 0u;
+    for (int k = 1; k < A; ++k) C[k] += (s < (uint32_t)k) ? 32u : 0u;
+    total += 32u;
   }
-  __device__ void halve() {
+  __device__ void halve() {  // codecs.py:234-242
     uint32_t prev = 0, t = 0;
 #pragma unroll
     for (int k = 1; k <= A; ++k) {
@@ -130,17 +67,39 @@ struct SModel<W, false> {  // A = 8, 16: cumulative counts in registers
     }
     total = t;
   }
+  // decode: s with C[s] <= target = min(x / unit, total - 1); returns unit*C[s], unit*C[s+1]
   __device__ __forceinline__ uint32_t find(uint32_t x, uint32_t unit, uint32_t& plo, uint32_t& phi) const {
-    uint32_t target = x / unit;
-    target = target < total - 1 ? target : total - 1;
-    uint32_t s = 0;
+    if constexpr (A <= 4) {
+      // x >= unit*C[k]  <=>  floor(x / unit) >= C[k]; the clamp to total-1 never
+      // changes the symbol because C[A-1] <= total - 1
+      uint32_t s = 0;
+      plo = 0;
+      phi = unit * C[1];
 #pragma unroll
-    for (int k = 1; k < A; ++k) s += (target >= C[k]) ? 1u : 0u;
-    uint32_t lo, hi;
-    lookup(s, lo, hi);
-    plo = unit * lo;
-    phi = unit * hi;
-    return s;
+      for (int k = 1; k < A; ++k) {
+        const uint32_t pk = unit * C[k];
+        const uint32_t pn = unit * (k + 1 < A ? C[k + 1] : total);
+        const bool ge = x >= pk;
+        s += ge ? 1u : 0u;
+        plo = ge ? pk : plo;
+        phi = ge ? pn : phi;
+      }
+      return s;
+    } else {
+      uint32_t target = x / unit;
+      target = target < total - 1 ? target : total - 1;
+      uint32_t s = 0, lo = 0, hi = C[1];
+#pragma unroll
+      for (int k = 1; k < A; ++k) {
+        const bool ge = target >= C[k];
+        s += ge ? 1u : 0u;
+        lo = ge ? C[k] : lo;
+        hi = ge ? (k + 1 < A ? C[k + 1] : total) : hi;
+      }
+      plo = unit * lo;
+      phi = unit * hi;
+      return s;
+    }
   }
 };
 
@@ -178,7 +137,7 @@ __device__ __forceinline__ uint32_t sym_at(const uint32_t* wd, int j) {
   return ((wd[k] << (off + W - 32)) | (wd[k + 1] >> (64 - off - W))) & mask;
 }
 
-// symbols per group and words per group: a group is a whole number of words
+// a group is a whole number of 32-bit words of symbols
 template <int W>
 struct Grp {
   static constexpr int kSyms = (W == 3) ? 32 : 32 / W;
@@ -213,18 +172,20 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
   constexpr int GS = Grp<W>::kSyms, GW = Grp<W>::kWords;
   const int n1 = min(n, kH) / GS;  // whole groups in the reciprocal-table phase
   for (int gI = 0; gI < n1; ++gI) {
-    uint32_t wd[GW];
+    uint32_t wd[GW], mg[GS];
 #pragma unroll
     for (int k = 0; k < GW; ++k) wd[k] = __byte_perm(__ldg(src + gI * GW + k), 0, 0x0123);
 #pragma unroll
+    for (int j = 0; j < GS; ++j) mg[j] = __ldg(magic + gI * GS + j);
+#pragma unroll
     for (int j = 0; j < GS; ++j) {
       const uint32_t s = sym_at<W>(wd, j);
-      const uint32_t unit = div_magic(e.range, m.total, magic[gI * GS + j]);
+      // m.total == A + 32*i until the first halving (warp-uniform)
+      const uint32_t unit = div_recip(e.range, m.total, mg[j]);
       uint32_t lo, hi;
       m.lookup(s, lo, hi);
       e.step(unit, lo, hi);
       m.add(s);
-      m.total += 32;
     }
   }
   int i = n1 * GS;
@@ -240,12 +201,11 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
       }
       nb -= W;
       const uint32_t s = (buf >> nb) & (A - 1);
-      const uint32_t unit = (i < kH) ? div_magic(e.range, m.total, magic[i]) : e.range / m.total;
+      const uint32_t unit = (i < kH) ? div_recip(e.range, m.total, __ldg(magic + i)) : e.range / m.total;
       uint32_t lo, hi;
       m.lookup(s, lo, hi);
       e.step(unit, lo, hi);
       m.add(s);
-      m.total += 32;
       if (m.total >= 65536u) m.halve();
     }
   }
@@ -259,15 +219,17 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
 // ----------------------------------------------------------------- decoder
 struct Dec {
   uint32_t low, range, code;
-  uint32_t cur;  // remaining bytes of the current input word, big-endian aligned at the top
-  int avail;     // bytes left in cur
-  const uint32_t* p;
-  const uint32_t* last;  // last readable word (reads are clamped; overruns are detected by count)
-  uint32_t pulled;       // bytes consumed after the 4 priming bytes
+  uint32_t cur;   // next input bytes, big-endian at the top
+  uint32_t avail; // bytes left in cur
+  uint32_t wi;    // index of the next word to load
+  uint32_t wlast; // last readable word (reads are clamped; overruns are detected by count)
+  uint32_t pulled;
+  const uint32_t* words;
   __device__ __forceinline__ uint32_t next_byte() {
+    ++pulled;
     if (avail == 0) {
-      p = p < last ? p + 1 : p;
-      cur = __byte_perm(__ldg(p), 0, 0x0123);
+      cur = __byte_perm(__ldg(words + min(wi, wlast)), 0, 0x0123);
+      ++wi;
       avail = 4;
     }
     const uint32_t b = cur >> 24;
@@ -285,7 +247,6 @@ struct Dec {
         range = (0u - low) & (kBot - 1u);
       }
       code = (code << 8) | next_byte();
-      ++pulled;
       low <<= 8;
       range <<= 8;
     }
@@ -294,25 +255,18 @@ struct Dec {
 
 template <int W>
 __device__ __forceinline__ uint32_t dec_symbol(Dec& d, SModel<W>& m, uint32_t unit) {
-  uint32_t s, plo, phi;
-  if (d.code >= d.low) {
-    s = m.find(d.code - d.low, unit, plo, phi);
-  } else {  // malformed stream: the reference's Fenwick search yields symbol 0
-    s = 0;
-    uint32_t lo, hi;
-    m.lookup(0, lo, hi);
-    plo = unit * lo;
-    phi = unit * hi;
-  }
+  // code < low only in a malformed stream; x = 0 then yields symbol 0 with
+  // the same bounds the reference's search gives for a negative target
+  const uint32_t x = d.code >= d.low ? d.code - d.low : 0u;
+  uint32_t plo, phi;
+  const uint32_t s = m.find(x, unit, plo, phi);
   d.step(plo, phi);
   m.add(s);
-  m.total += 32;
   return s;
 }
 
 template <int W>
 __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
-  constexpr int A = 1 << W;
   const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const StreamTab st = *a.st;
@@ -340,14 +294,17 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   d.code = code;
   d.pulled = 0;
   {
-    const uintptr_t q = reinterpret_cast<uintptr_t>(src + 8);
-    const uintptr_t e = reinterpret_cast<uintptr_t>(a.payload_in + o1 - 1);
-    d.p = reinterpret_cast<const uint32_t*>(q & ~(uintptr_t)3);
-    d.last = reinterpret_cast<const uint32_t*>(e & ~(uintptr_t)3);
-    if (d.p > d.last) d.p = d.last;
-    const int skip = (int)(q & 3);
-    d.cur = __byte_perm(__ldg(d.p), 0, 0x0123) << (8 * skip);
+    // words are indexed from the aligned word holding src+4 (always inside the
+    // block); every load is clamped to the word holding the block's last byte
+    const uintptr_t base = reinterpret_cast<uintptr_t>(src + 4) & ~(uintptr_t)3;
+    const uintptr_t last = reinterpret_cast<uintptr_t>(a.payload_in + o1 - 1) & ~(uintptr_t)3;
+    const uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(src + 8) - base);
+    d.words = reinterpret_cast<const uint32_t*>(base);
+    d.wlast = (uint32_t)((last - base) >> 2);
+    const uint32_t w0 = off >> 2, skip = off & 3;
+    d.cur = __byte_perm(__ldg(d.words + min(w0, d.wlast)), 0, 0x0123) << (8 * skip);
     d.avail = 4 - skip;
+    d.wi = w0 + 1;
   }
   SModel<W> m;
   m.init();
@@ -357,16 +314,19 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   const int n1 = aligned ? min(n, kH) / GS : 0;
   uint32_t* dw = reinterpret_cast<uint32_t*>(dst);
   for (int gI = 0; gI < n1; ++gI) {
+    uint32_t mg[GS];
+#pragma unroll
+    for (int j = 0; j < GS; ++j) mg[j] = __ldg(magic + gI * GS + j);
     uint64_t acc = 0;
-    int nbits = 0, wi = 0;  // compile-time after unrolling
+    int nbits = 0, wo = 0;  // compile-time after unrolling
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      const uint32_t unit = div_magic(d.range, m.total, magic[gI * GS + j]);
+      const uint32_t unit = div_recip(d.range, m.total, mg[j]);
       acc = (acc << W) | dec_symbol<W>(d, m, unit);
       nbits += W;
       if (nbits >= 32) {
         nbits -= 32;
-        dw[gI * GW + wi++] = __byte_perm((uint32_t)(acc >> nbits), 0, 0x0123);
+        dw[gI * GW + wo++] = __byte_perm((uint32_t)(acc >> nbits), 0, 0x0123);
       }
     }
   }
@@ -375,7 +335,7 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   uint64_t acc = 0;
   int nacc = 0, nout = i * W / 8;
   for (; i < n; ++i) {
-    const uint32_t unit = (i < kH) ? div_magic(d.range, m.total, magic[i]) : d.range / m.total;
+    const uint32_t unit = (i < kH) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
     acc = (acc << W) | dec_symbol<W>(d, m, unit);
     if (m.total >= 65536u) m.halve();
     nacc += W;
@@ -384,7 +344,8 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
       dst[nout++] = (uint8_t)(acc >> nacc);
     }
   }
-  // reading past the block's bytes is a truncated stream (codecs.py:283-288)
+  // bytes consumed = 4 header + 4 priming + pulled; pulling past the block is
+  // a truncated stream (codecs.py:283-288)
   if ((uint64_t)d.pulled + 8 > o1 - o0) atomicOr(a.status, KVC_FLAG_CODEC);
 }
 
