@@ -426,7 +426,9 @@ static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payloa
   a.page_tokens = page_tokens;
   a.layer_stride = layer_stride;
   fill_common(p, a.hk, a.hc);
-  if (fast128_applicable(g))
+  if (delta128_applicable(g))
+    e = launch_decode_delta128(a, s);
+  else if (fast128_applicable(g))
     e = launch_decode_fast128(a, p.sm_count, s);
   else if (uchan128_applicable(g))
     e = launch_decode_uchan128(a, p.sm_count, s);

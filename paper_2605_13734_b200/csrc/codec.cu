@@ -21,54 +21,91 @@ namespace kvc {
 namespace {
 
 // ----------------------------------------------------------------- RLE
-__device__ void rle_encode_block(const uint8_t* src, int64_t n, uint8_t* slot, int64_t cap, uint64_t* size_out,
+// 16-byte vector reader (byte loads when the range is not 16-byte aligned,
+// e.g. tiny blocks of odd widths)
+struct VecReader {
+  const uint4* p;
+  const uint8_t* bp;
+  uint4 cur;
+  int idx;  // next byte within cur (0..16)
+  bool vec;
+  __device__ __forceinline__ void init(const uint8_t* src) {
+    p = reinterpret_cast<const uint4*>(src);
+    bp = src;
+    vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    idx = 16;
+  }
+  __device__ __forceinline__ uint32_t next() {
+    if (!vec) return __ldg(bp++);
+    if (idx == 16) {
+      cur = __ldg(p++);
+      idx = 0;
+    }
+    const uint32_t w = (idx < 8) ? ((idx < 4) ? cur.x : cur.y) : ((idx < 12) ? cur.z : cur.w);
+    const uint32_t b = (w >> (8 * (idx & 3))) & 0xFFu;
+    ++idx;
+    return b;
+  }
+};
+
+__device__ void rle_encode_block(const uint8_t* src, int n, uint8_t* slot, int64_t cap, uint64_t* size_out,
                                  uint32_t* status) {
-  // greedy PackBits (codecs.py:112-152): runs >= 3 become (128+len-3, byte)
-  // in chunks <= 130; everything else is literal in chunks <= 128.
-  int64_t pos = 0;
-  int64_t i = 0;
-  int64_t lit = -1;
-  auto emit_lit = [&](int64_t from, int64_t upto) {
-    while (from < upto) {
-      int64_t ch = upto - from < 128 ? upto - from : 128;
-      if (pos + 1 + ch <= cap) {
-        slot[pos] = (uint8_t)(ch - 1);
-        for (int64_t k = 0; k < ch; ++k) slot[pos + 1 + k] = src[from + k];
-      }
-      pos += 1 + ch;
-      from += ch;
+  // greedy PackBits (codecs.py:112-152), single pass: runs >= 3 become
+  // (128+len-3, byte) in chunks <= 130; all other bytes go into literal
+  // chunks <= 128 whose control byte is back-filled when the chunk closes.
+  // Output <= n + ceil(n/128) bytes, within the slot by construction.
+  (void)cap;
+  (void)status;
+  VecReader rd;
+  rd.init(src);
+  int pos = 0;         // output position
+  int lit_ctrl = -1;   // position of the open literal chunk's control byte
+  int lit_len = 0;
+  auto lit_byte = [&](uint32_t b) {
+    if (lit_ctrl < 0 || lit_len == 128) {
+      if (lit_ctrl >= 0) slot[lit_ctrl] = (uint8_t)(lit_len - 1);
+      lit_ctrl = pos++;
+      lit_len = 0;
     }
+    slot[pos++] = (uint8_t)b;
+    ++lit_len;
   };
+  auto lit_close = [&]() {
+    if (lit_ctrl >= 0) slot[lit_ctrl] = (uint8_t)(lit_len - 1);
+    lit_ctrl = -1;
+    lit_len = 0;
+  };
+  int i = 0;
+  uint32_t v = n > 0 ? rd.next() : 0u;
   while (i < n) {
-    const uint8_t v = src[i];
-    int64_t j = i + 1;
-    while (j < n && src[j] == v) ++j;
-    int64_t run = j - i;
-    if (run >= 3) {
-      if (lit >= 0) {
-        emit_lit(lit, i);
-        lit = -1;
+    int run = 1;
+    uint32_t nb = 0;
+    bool more = false;
+    while (i + run < n) {
+      nb = rd.next();
+      if (nb != v) {
+        more = true;
+        break;
       }
-      while (run >= 3) {
-        int64_t ch = run < 130 ? run : 130;
-        if (pos + 2 <= cap) {
-          slot[pos] = (uint8_t)(128 + ch - 3);
-          slot[pos + 1] = v;
-        }
-        pos += 2;
-        run -= ch;
-      }
-      if (run) lit = j - run;
-    } else if (lit < 0) {
-      lit = i;
+      ++run;
     }
-    i = j;
+    if (run >= 3) {
+      lit_close();
+      int r = run;
+      while (r >= 3) {
+        const int ch = r < 130 ? r : 130;
+        slot[pos++] = (uint8_t)(128 + ch - 3);
+        slot[pos++] = (uint8_t)v;
+        r -= ch;
+      }
+      for (int k = 0; k < r; ++k) lit_byte(v);  // leftover < 3 starts a literal
+    } else {
+      for (int k = 0; k < run; ++k) lit_byte(v);
+    }
+    i += run;
+    if (more) v = nb;
   }
-  if (lit >= 0) emit_lit(lit, n);
-  if (pos > cap) {
-    atomicOr(status, KVC_FLAG_CAPACITY);
-    pos = 0;
-  }
+  lit_close();
   *size_out = (uint64_t)pos;
 }
 
@@ -107,26 +144,64 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
     return;
   }
   const uint8_t* in = a.payload_in + o0;
-  const int64_t len = (int64_t)(o1 - o0);
+  const int len = (int)(o1 - o0);
   uint8_t* out = a.packed_out + st.byte_off[si] + start * w / 8;
-  int64_t pos = 0, o = 0;
+  // input: aligned words, clamped to the word holding the block's last byte
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uint32_t* iw = reinterpret_cast<const uint32_t*>(ia & ~(uintptr_t)3);
+  const int ilast = len > 0 ? (int)(((ia + len - 1) & ~(uintptr_t)3) - (ia & ~(uintptr_t)3)) / 4 : 0;
+  int wi = 0, avail = 0;
+  uint32_t cur = 0;
+  int skip = (int)(ia & 3);
+  auto rd = [&]() -> uint32_t {
+    if (avail == 0) {
+      cur = __ldg(iw + min(wi, ilast)) >> (8 * skip);
+      avail = 4 - skip;
+      skip = 0;
+      ++wi;
+    }
+    const uint32_t b = cur & 0xFFu;
+    cur >>= 8;
+    --avail;
+    return b;
+  };
+  // output: little-endian word accumulator (the block start is 4-aligned)
+  const bool oal = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  uint32_t acc = 0;
+  int o = 0;
+  auto wr = [&](uint32_t b) {
+    if (oal) {
+      acc |= b << (8 * (o & 3));
+      if ((o & 3) == 3) {
+        reinterpret_cast<uint32_t*>(out)[o >> 2] = acc;
+        acc = 0;
+      }
+    } else {
+      out[o] = (uint8_t)b;
+    }
+    ++o;
+  };
+  int pos = 0;
   bool bad = false;
   while (pos < len) {  // codecs.py:155-174
-    uint32_t c = in[pos++];
+    const uint32_t c = rd();
+    ++pos;
     if (c < 128) {
-      int64_t l = (int64_t)c + 1;
+      const int l = (int)c + 1;
       if (pos + l > len || o + l > want) { bad = true; break; }
-      for (int64_t k = 0; k < l; ++k) out[o + k] = in[pos + k];
-      o += l;
+      for (int k = 0; k < l; ++k) wr(rd());
       pos += l;
     } else {
       if (pos >= len) { bad = true; break; }
-      int64_t l = (int64_t)c - 125;
+      const int l = (int)c - 125;
       if (o + l > want) { bad = true; break; }
-      const uint8_t v = in[pos++];
-      for (int64_t k = 0; k < l; ++k) out[o + k] = v;
-      o += l;
+      const uint32_t v = rd();
+      ++pos;
+      for (int k = 0; k < l; ++k) wr(v);
     }
+  }
+  if (oal && (o & 3)) {  // partial last word: bytes only (a neighbour may own the rest)
+    for (int k = 0; k < (o & 3); ++k) out[(o & ~3) + k] = (uint8_t)(acc >> (8 * k));
   }
   if (bad || o != want) atomicOr(a.status, KVC_FLAG_CODEC);
 }

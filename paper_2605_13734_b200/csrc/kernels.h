@@ -81,6 +81,10 @@ bool uchan128_applicable(const Geo& g);
 cudaError_t launch_encode_uchan128(const EncArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_decode_uchan128(const DecArgs& a, int sm_count, cudaStream_t s);
 
+// delta decode, head_dim 128, exact sequential fp64 cumsum (delta128.cu)
+bool delta128_applicable(const Geo& g);
+cudaError_t launch_decode_delta128(const DecArgs& a, cudaStream_t s);
+
 // small-alphabet range coder (rc_small.cu), widths 1..4
 bool rc_small_supported(int w);
 cudaError_t launch_rc_small_encode(const CodecArgs& a, int w, unsigned grid, cudaStream_t s);
