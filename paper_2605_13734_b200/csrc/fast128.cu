@@ -160,51 +160,66 @@ __device__ __forceinline__ void unpack32_dispatch(int w, const uint8_t* src, flo
 }
 
 // ------------------------------------------------------------ group stats
+// min / max of 32 fp32 values
+__device__ __forceinline__ void minmax32(const float* y, float& mn, float& mx) {
+  mn = y[0];
+  mx = y[0];
+#pragma unroll
+  for (int i = 1; i < 32; ++i) {
+    mn = fminf(mn, y[i]);
+    mx = fmaxf(mx, y[i]);
+  }
+}
+
+// min / max of 32 bf16 values packed in 16 words: two per HMNMX2, exact, and
+// NaN-propagating so a NaN input surfaces in the group stats (the reference
+// rejects non-finite values, tensors.py:41-42)
+__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ void minmax32_bf16(const uint32_t* w, float& mn, float& mx) {
+  uint32_t lo = w[0], hi = w[0];
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {
+    lo = bmin2(lo, w[k]);
+    hi = bmax2(hi, w[k]);
+  }
+  lo = bmin2(lo, __byte_perm(lo, 0, 0x1032));  // both halves now hold the min
+  hi = bmax2(hi, __byte_perm(hi, 0, 0x1032));
+  mn = __uint_as_float(lo << 16);
+  mx = __uint_as_float(hi << 16);
+}
+
+// true iff any of the 64 bf16 values packed in w[0..31] is NaN or +-inf
+__device__ __forceinline__ bool nonfinite64_bf16(const uint32_t* w) {
+  uint32_t m = w[0] & 0x7FFF7FFFu;
+#pragma unroll
+  for (int k = 1; k < 32; ++k) m = bmax2(m, w[k] & 0x7FFF7FFFu);
+  return ((m & 0x7F80u) == 0x7F80u) | ((m & 0x7F800000u) == 0x7F800000u);
+}
+
 // Quantize the thread's 64 values (two chunks of 32 at channel bases cb0,
-// cb1), group size G in {8,16,32,64,128}; `xchg` = the partner thread holds
-// the other half of a 64/128 group (hadamard layout or G = 128).
+// cb1) given each chunk's min/max; G in {32, 64, 128}: a 64-group is both
+// chunks (natural layout) or chunk c of both threads of the row (hadamard
+// layout); a 128-group is the whole row across the thread pair.
 template <int G>
-__device__ __forceinline__ void quantize64(float* y, int cb0, int cb1, int w, float rl, int64_t grow,
-                                           __half* scales, __half* zeros, bool hadlayout, int half,
-                                           uint32_t& flags) {
-  if constexpr (G <= 32) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-#pragma unroll
-      for (int j = 0; j < 32 / G; ++j) {
-        float* yy = y + c * 32 + j * G;
-        float mn = yy[0], mx = yy[0];
-#pragma unroll
-        for (int i = 1; i < G; ++i) {
-          mn = fminf(mn, yy[i]);
-          mx = fmaxf(mx, yy[i]);
-        }
-        __half s16, z16;
-        GroupQ q = group_setup(mn, mx, w, rl, s16, z16, flags);
-        const int64_t gi = grow + ((c ? cb1 : cb0) + j * G) / G;
-        if (scales) {
-          scales[gi] = s16;
-          zeros[gi] = z16;
-        }
-        if (q.mode == 0) {
-#pragma unroll
-          for (int i = 0; i < G; ++i) yy[i] = quant_magic(yy[i], q);
-        } else {
-#pragma unroll
-          for (int i = 0; i < G; ++i) yy[i] = __uint_as_float(kMagicBits + quant_one(yy[i], q));
-        }
-      }
-    }
-  } else {
-    // G = 64 or 128: stats over both chunks and/or the partner thread
-    float mn0 = y[0], mx0 = y[0], mn1 = y[32], mx1 = y[32];
-#pragma unroll
-    for (int i = 1; i < 32; ++i) {
-      mn0 = fminf(mn0, y[i]); mx0 = fmaxf(mx0, y[i]);
-      mn1 = fminf(mn1, y[32 + i]); mx1 = fmaxf(mx1, y[32 + i]);
-    }
+__device__ __forceinline__ void quantize64(float* y, float mn0, float mx0, float mn1, float mx1, int cb0, int cb1,
+                                           int w, float rl, int64_t grow, __half* scales, __half* zeros,
+                                           bool hadlayout, int half, uint32_t& flags) {
+  static_assert(G == 32 || G == 64 || G == 128, "fused path groups");
+  {
     float gmn[2], gmx[2];
-    if (G == 128) {
+    if (G == 32) {
+      gmn[0] = mn0; gmx[0] = mx0;
+      gmn[1] = mn1; gmx[1] = mx1;
+    } else if (G == 128) {
       float mn = fminf(mn0, mn1), mx = fmaxf(mx0, mx1);
       mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -225,7 +240,7 @@ __device__ __forceinline__ void quantize64(float* y, int cb0, int cb1, int w, fl
       GroupQ q = group_setup(gmn[c], gmx[c], w, rl, s16, z16, flags);
       const int64_t gi = grow + (c ? cb1 : cb0) / G;
       // one writer per group
-      const bool writer = (G == 128) ? (half == 0 && c == 0) : (!hadlayout ? c == 0 : (half == c));
+      const bool writer = (G == 32) ? true : (G == 128) ? (half == 0 && c == 0) : (!hadlayout ? c == 0 : (half == c));
       if (writer && scales) {
         scales[gi] = s16;
         zeros[gi] = z16;
@@ -323,6 +338,9 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     int cb0, cb1;
     bool hadlayout = false;
     if (MODE == M_HADAMARD) {
+      // the 2^-896 reinterpretation maps NaN / inf to finite doubles: check the
+      // bf16 input explicitly (tensors.py:41-42)
+      if (nonfinite64_bf16(wv)) nanacc = 1.0f;
       double f[64];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -387,8 +405,6 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
         y[2 * j] = __uint_as_float(wv[j] << 16);
         y[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
       }
-#pragma unroll
-      for (int i = 0; i < 64; ++i) nanacc = __fmaf_rn(y[i], 0.0f, nanacc);
       if (MODE == M_DELTA && t > 0) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -414,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
         }
       }
       if (MODE == M_DELTA || MODE == M_AFFINE) {
+        // a non-finite input or transform result (tensors.py:41-42) shows up here
         float chk = 0.0f;
 #pragma unroll
         for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
@@ -422,11 +439,22 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       cb0 = 64 * half;
       cb1 = 64 * half + 32;
     }
+    float mn0, mx0, mn1, mx1;
+    if (MODE == M_IDENTITY) {
+      // exact bf16 min/max, two per instruction; NaN / inf surface here
+      minmax32_bf16(wv, mn0, mx0);
+      minmax32_bf16(wv + 16, mn1, mx1);
+      if (!(isfinite(mn0) && isfinite(mx0) && isfinite(mn1) && isfinite(mx1))) nanacc = 1.0f;
+    } else {
+      minmax32(y, mn0, mx0);
+      minmax32(y + 32, mn1, mx1);
+    }
 
     int w;
     int64_t bit;
     token_row_pos(g, a.heads, lh, t, w, bit);
-    quantize64<G>(y, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros, hadlayout, half, flags);
+    quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
+                  hadlayout, half, flags);
     if (valid) {
       uint8_t* out = a.packed + (bit >> 3);
       if constexpr (W == 0) {

@@ -88,10 +88,18 @@ def test_decompress_rejects_mismatched_strategy():  # test_compress.py:82-95
 def test_nonfinite_input_raises_value_error():  # tensors.py:41-42
     from paper_2605_13734_b200 import KVTensor, compress
 
-    v = torch.randn(1, 2, 8, 128, device="cuda", dtype=torch.bfloat16)
-    v[0, 1, 3, 7] = float("nan")
+    for sid in ("t=identity;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=4,g=32;c=none",
+                "t=delta;q=uniform,b=2,g=64;c=entropy", "t=affine;q=uniform,b=8,g=32;c=none",
+                "t=identity;q=uchan,b=2,g=32;c=none", "t=hadamard;q=mixed,hi=8,lo=2,g=128,rho=0.25;c=rle"):
+        for bad in (float("nan"), float("inf"), float("-inf")):
+            v = torch.randn(1, 2, 128, 128, device="cuda", dtype=torch.bfloat16)
+            v[0, 1, 37, 7] = bad
+            with pytest.raises(ValueError):
+                compress(KVTensor(v), sid)
+    v = torch.randn(1, 2, 8, 64, device="cuda", dtype=torch.bfloat16)  # generic path
+    v[0, 0, 2, 5] = float("nan")
     with pytest.raises(ValueError):
-        compress(KVTensor(v), "t=identity;q=uniform,b=4,g=32;c=none")
+        compress(KVTensor(v), "t=hadamard;q=uniform,b=4,g=32;c=none")
     with pytest.raises(ValueError):
         KVTensor(np.full((1, 1, 2, 4), np.inf, np.float32))
 
