@@ -1,0 +1,163 @@
+// Range coder state machines shared by the small- and large-alphabet coders
+// (codecs.py:245-307: 32-bit carry-less coder, TOP = 2^24, BOTTOM = 2^16).
+//
+// The reference renormalizes one byte per loop iteration.  On a GPU that
+// loop diverges across the lanes of a warp (each lane codes its own block),
+// so the common case is done in closed form: after `low += unit*cum; range =
+// unit*freq` the bytes the loop would shift out while the top bytes of low
+// and low + range agree are exactly the leading equal bytes,
+//   k = carry ? 0 : clz(low ^ (low + range)) / 8      (0..3),
+// because shifting a carry-free pair keeps it carry-free.  Those k bytes move
+// in one step; only the rare underflow case (top bytes differ but range <
+// BOTTOM, codecs.py:258-259) falls back to the reference's byte loop.
+#pragma once
+#include <stdint.h>
+
+namespace kvc {
+
+constexpr uint32_t kRcTop = 1u << 24;
+constexpr uint32_t kRcBot = 1u << 16;
+
+__device__ __forceinline__ uint32_t rc_settled_bytes(uint32_t low, uint32_t range) {
+  const uint32_t t = low + range;
+  return t < low ? 0u : (__clz(low ^ t) >> 3);
+}
+
+// Encoder: output bytes accumulate in a 64-bit window (newest byte lowest)
+// and are stored one big-endian word at a time.
+struct RcEnc {
+  uint32_t low, range;
+  uint32_t whi, wlo;
+  uint32_t nb;    // bits emitted
+  uint32_t* out;
+
+  __device__ __forceinline__ void init(uint32_t* o) {
+    low = 0;
+    range = 0xFFFFFFFFu;
+    whi = wlo = 0;
+    nb = 0;
+    out = o;
+  }
+  // shift the top k <= 3 bytes of low out (codecs.py:261-263, k times)
+  __device__ __forceinline__ void put(uint32_t k) {
+    const uint32_t sh = 8u * k;
+    const uint32_t bytes = __funnelshift_l(low, 0u, sh);  // low >> (32 - sh), 0 for k = 0
+    whi = __funnelshift_l(wlo, whi, sh);
+    wlo = (wlo << sh) | bytes;
+    const uint32_t o = nb;
+    nb += sh;
+    if ((nb ^ o) >= 32u) out[(nb >> 5) - 1] = __byte_perm(__funnelshift_r(wlo, whi, nb), 0, 0x0123);
+    low <<= sh;
+    range <<= sh;
+  }
+  __device__ __forceinline__ void underflow() {  // the reference's loop, from a settled state
+    for (;;) {
+      const uint32_t t = low + range;
+      if (t < low || (low ^ t) >= kRcTop) {
+        if (range >= kRcBot) break;
+        range = (0u - low) & (kRcBot - 1u);
+      }
+      put(1);
+    }
+  }
+  __device__ __forceinline__ void encode(uint32_t unit, uint32_t cum, uint32_t freq) {
+    low += unit * cum;
+    range = unit * freq;
+    put(rc_settled_bytes(low, range));
+    if (range < kRcBot) underflow();
+  }
+  // finish (codecs.py:266-270): four bytes of low, then the partial word;
+  // returns the byte count
+  __device__ __forceinline__ uint32_t finish() {
+    put(3);
+    put(1);
+    const uint32_t r = nb & 31u;
+    if (r) out[nb >> 5] = __byte_perm(wlo << (32u - r), 0, 0x0123);
+    return nb >> 3;
+  }
+};
+
+// Decoder: input bytes come from a 64-bit window (next byte at the top of
+// hi) refilled one aligned word at a time; reads are clamped to the block's
+// last word and an overrun shows up as pulled > available.
+struct RcDec {
+  uint32_t low, range, code;
+  uint32_t hi, lo;
+  uint32_t avail;  // bytes in the window; >= 4 between symbols
+  uint32_t wi, wlast, skip;
+  const uint32_t* words;
+
+  __device__ __forceinline__ uint32_t load() {
+    const uint32_t w = __byte_perm(__ldg(words + min(wi, wlast)), 0, 0x0123);
+    ++wi;
+    return w;
+  }
+  __device__ __forceinline__ void refill() {
+    if (avail < 4u) {  // avail in 1..3 here
+      const uint32_t w = load();
+      hi |= w >> (8u * avail);
+      lo = w << (32u - 8u * avail);
+      avail += 4u;
+    }
+  }
+  // block = [BE32 length][range-coded bytes]; bytes [o0, o1) of the payload
+  __device__ __forceinline__ void init(const uint8_t* blk, const uint8_t* blk_end) {
+    const uintptr_t base = reinterpret_cast<uintptr_t>(blk + 4) & ~(uintptr_t)3;
+    const uintptr_t last = reinterpret_cast<uintptr_t>(blk_end - 1) & ~(uintptr_t)3;
+    words = reinterpret_cast<const uint32_t*>(base);
+    wlast = (uint32_t)((last - base) >> 2);
+    skip = (uint32_t)(reinterpret_cast<uintptr_t>(blk + 4) - base);  // 0..3
+    wi = 0;
+    hi = load() << (8u * skip);
+    const uint32_t w1 = load();
+    if (skip == 0) {
+      lo = w1;
+      avail = 8u;
+    } else {
+      hi |= w1 >> (32u - 8u * skip);
+      lo = w1 << (8u * skip);
+      avail = 8u - skip;
+    }
+    // the first four bytes prime `code` (codecs.py:280-281)
+    code = hi;
+    hi = lo;
+    lo = 0;
+    avail -= 4u;  // 1..4
+    refill();
+    low = 0;
+    range = 0xFFFFFFFFu;
+  }
+  // pull k <= 3 bytes into code (codecs.py:303-305, k times)
+  __device__ __forceinline__ void take(uint32_t k) {
+    const uint32_t sh = 8u * k;
+    code = (code << sh) | __funnelshift_l(hi, 0u, sh);
+    hi = __funnelshift_l(lo, hi, sh);
+    lo <<= sh;
+    avail -= k;
+    low <<= sh;
+    range <<= sh;
+    refill();
+  }
+  // stream bytes consumed after the 4 priming bytes
+  __device__ __forceinline__ uint32_t pulled() const { return 4u * wi - skip - 4u - avail; }
+  __device__ __forceinline__ void underflow() {
+    for (;;) {
+      const uint32_t t = low + range;
+      if (t < low || (low ^ t) >= kRcTop) {
+        if (range >= kRcBot) break;
+        range = (0u - low) & (kRcBot - 1u);
+      }
+      take(1);
+    }
+  }
+  // code - low (codecs.py:290-292); a malformed stream with code < low reads 0
+  __device__ __forceinline__ uint32_t offset() const { return code >= low ? code - low : 0u; }
+  __device__ __forceinline__ void advance(uint32_t plo, uint32_t phi) {  // plo = unit*cum, phi = unit*(cum+freq)
+    low += plo;
+    range = phi - plo;
+    take(rc_settled_bytes(low, range));
+    if (range < kRcBot) underflow();
+  }
+};
+
+}  // namespace kvc

@@ -16,13 +16,12 @@
 
 #include "kernels.h"
 #include "profile.h"
+#include "rc_coder.cuh"
 #include "rc_tables.cuh"
 
 namespace kvc {
 namespace {
 
-constexpr uint32_t kTop = 1u << 24;
-constexpr uint32_t kBot = 1u << 16;
 constexpr int kLThreads = 128;
 
 template <int W>
@@ -136,7 +135,8 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
   uint32_t* out = reinterpret_cast<uint32_t*>(slot + 4);
   LModel<W> m;
   m.init(lsm, threadIdx.x);
-  uint32_t low = 0, range = 0xFFFFFFFFu, acc = 0, nout = 0;
+  RcEnc e;
+  e.init(out);
   uint32_t buf = 0;
   int nb = 0, pos = 0;
   for (int i = 0; i < n; ++i) {
@@ -148,35 +148,17 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
     const uint32_t s = (buf >> nb) & (A - 1);
     const uint32_t cum = m.prefix(s);
     const uint32_t fr = m.freq(s);
-    const uint32_t unit = (i < H) ? div_recip(range, m.total, __ldg(magic + i)) : range / m.total;
-    low += unit * cum;
-    range = unit * fr;
-    for (;;) {
-      const uint32_t t = low + range;
-      if (t < low || (low ^ t) >= kTop) {
-        if (range >= kBot) break;
-        range = (0u - low) & (kBot - 1u);
-      }
-      acc = __funnelshift_l(low, acc, 8);
-      if ((++nout & 3u) == 0) out[(nout >> 2) - 1] = __byte_perm(acc, 0, 0x0123);
-      low <<= 8;
-      range <<= 8;
-    }
+    const uint32_t unit = (i < H) ? div_recip(e.range, m.total, __ldg(magic + i)) : e.range / m.total;
+    e.encode(unit, cum, fr);
     m.bump(s);
   }
-  for (int k = 0; k < 4; ++k) {
-    acc = __funnelshift_l(low, acc, 8);
-    if ((++nout & 3u) == 0) out[(nout >> 2) - 1] = __byte_perm(acc, 0, 0x0123);
-    low <<= 8;
-  }
-  if (nout & 3u) out[nout >> 2] = __byte_perm(acc << (8 * (4 - (nout & 3u))), 0, 0x0123);
+  const uint32_t nout = e.finish();
   *reinterpret_cast<uint32_t*>(slot) = __byte_perm(nout, 0, 0x0123);
   a.sizes[b] = (uint64_t)nout + 4;
 }
 
 template <int W>
 __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
-  constexpr int A = 1 << W;
   constexpr int H = halving_at<W>();
   extern __shared__ __align__(16) uint16_t lsm[];
   const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
@@ -194,26 +176,24 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   }
   const uint8_t* src = a.payload_in + o0;
   const int64_t len = (int64_t)(o1 - o0);
-  uint32_t hdr = 0, code = 0;
+  uint32_t hdr = 0;
   for (int k = 0; k < 4; ++k) hdr = (hdr << 8) | src[k];
   if ((int64_t)hdr + 4 != len) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
-  for (int k = 4; k < 8; ++k) code = (code << 8) | src[k];
-  int64_t rp = 8;
-  bool bad = false;
+  RcDec d;
+  d.init(src, src + len);
   LModel<W> m;
   m.init(lsm, threadIdx.x);
   uint8_t* dst = a.packed_out + st.byte_off[si] + start * W / 8;
-  uint32_t low = 0, range = 0xFFFFFFFFu;
   uint64_t acc = 0;
   int nacc = 0, nout = 0;
   for (int i = 0; i < n; ++i) {
-    const uint32_t unit = (i < H) ? div_recip(range, m.total, __ldg(magic + i)) : range / m.total;
+    const uint32_t unit = (i < H) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
     uint32_t s, cum;
-    if (code >= low) {
-      uint32_t target = (code - low) / unit;
+    if (d.code >= d.low) {
+      uint32_t target = (d.code - d.low) / unit;
       target = target < m.total - 1 ? target : m.total - 1;
       s = m.find(target, cum);
     } else {  // malformed stream: the reference's search yields symbol 0
@@ -221,22 +201,7 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
       cum = 0;
     }
     const uint32_t fr = m.freq(s);
-    low += unit * cum;
-    range = unit * fr;
-    for (;;) {
-      const uint32_t t = low + range;
-      if (t < low || (low ^ t) >= kTop) {
-        if (range >= kBot) break;
-        range = (0u - low) & (kBot - 1u);
-      }
-      uint32_t byte = 0;
-      if (rp < len) byte = src[rp];
-      else bad = true;
-      ++rp;
-      code = (code << 8) | byte;
-      low <<= 8;
-      range <<= 8;
-    }
+    d.advance(unit * cum, unit * (cum + fr));
     m.bump(s);
     acc = (acc << W) | s;
     nacc += W;
@@ -245,7 +210,8 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
       dst[nout++] = (uint8_t)(acc >> nacc);
     }
   }
-  if (bad) atomicOr(a.status, KVC_FLAG_CODEC);
+  // bytes consumed = 4 header + 4 priming + pulled (codecs.py:283-288)
+  if ((int64_t)d.pulled() + 8 > len) atomicOr(a.status, KVC_FLAG_CODEC);
 }
 
 template <int W>

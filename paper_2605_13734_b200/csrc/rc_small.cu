@@ -14,19 +14,18 @@
 // run a generic per-symbol loop with hardware division.  Cumulative
 // frequencies C[1..A-1] live in registers; lookup and update share the
 // predicates (s >= k); the decoder's symbol search for A <= 4 is branch-free
-// (compare x = code - low against unit * C[k]).  Bytes are emitted / pulled
-// with one funnel shift each.
+// (compare x = code - low against unit * C[k]).  Renormalization moves all
+// settled bytes in one branch-free step (rc_coder.cuh).
 #include <cstdint>
 
 #include "kernels.h"
 #include "profile.h"
+#include "rc_coder.cuh"
 #include "rc_tables.cuh"
 
 namespace kvc {
 namespace {
 
-constexpr uint32_t kTop = 1u << 24;
-constexpr uint32_t kBot = 1u << 16;
 constexpr int kH = 2048;  // first halving after symbol kH-1 for every A in 2..16
 
 template <int W>
@@ -103,32 +102,6 @@ struct SModel {
   }
 };
 
-// ----------------------------------------------------------------- encoder
-struct Enc {
-  uint32_t low, range;
-  uint32_t acc;  // pending output bytes, big-endian
-  uint32_t n;    // bytes emitted
-  uint32_t* out;
-  __device__ __forceinline__ void emit() {
-    acc = __funnelshift_l(low, acc, 8);  // acc << 8 | low >> 24
-    if ((++n & 3u) == 0) out[(n >> 2) - 1] = __byte_perm(acc, 0, 0x0123);
-    low <<= 8;
-    range <<= 8;
-  }
-  __device__ __forceinline__ void step(uint32_t unit, uint32_t lo, uint32_t hi) {
-    low += unit * lo;
-    range = unit * (hi - lo);
-    for (;;) {  // codecs.py:255-264, (low ^ (low + range)) < TOP in 33 bits
-      const uint32_t t = low + range;
-      if (t < low || (low ^ t) >= kTop) {
-        if (range >= kBot) break;
-        range = (0u - low) & (kBot - 1u);
-      }
-      emit();
-    }
-  }
-};
-
 template <int W>
 __device__ __forceinline__ uint32_t sym_at(const uint32_t* wd, int j) {
   constexpr uint32_t mask = (1u << W) - 1u;
@@ -163,12 +136,8 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
   uint8_t* slot = a.slots + b * a.slot_bytes;
   SModel<W> m;
   m.init();
-  Enc e;
-  e.low = 0;
-  e.range = 0xFFFFFFFFu;
-  e.acc = 0;
-  e.n = 0;
-  e.out = reinterpret_cast<uint32_t*>(slot + 4);
+  RcEnc e;
+  e.init(reinterpret_cast<uint32_t*>(slot + 4));
   constexpr int GS = Grp<W>::kSyms, GW = Grp<W>::kWords;
   const int n1 = min(n, kH) / GS;  // whole groups in the reciprocal-table phase
   for (int gI = 0; gI < n1; ++gI) {
@@ -184,7 +153,7 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
       const uint32_t unit = div_recip(e.range, m.total, mg[j]);
       uint32_t lo, hi;
       m.lookup(s, lo, hi);
-      e.step(unit, lo, hi);
+      e.encode(unit, lo, hi - lo);
       m.add(s);
     }
   }
@@ -204,63 +173,24 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
       const uint32_t unit = (i < kH) ? div_recip(e.range, m.total, __ldg(magic + i)) : e.range / m.total;
       uint32_t lo, hi;
       m.lookup(s, lo, hi);
-      e.step(unit, lo, hi);
+      e.encode(unit, lo, hi - lo);
       m.add(s);
       if (m.total >= 65536u) m.halve();
     }
   }
-  for (int k = 0; k < 4; ++k) e.emit();  // finish: 4 bytes of low (codecs.py:266-270)
-  if (e.n & 3u) e.out[e.n >> 2] = __byte_perm(e.acc << (8 * (4 - (e.n & 3u))), 0, 0x0123);
-  const uint32_t len = e.n;  // <= 4 bytes per symbol + 4 < slot capacity
+  const uint32_t len = e.finish();  // <= 4 bytes per symbol + 4 < slot capacity
   *reinterpret_cast<uint32_t*>(slot) = __byte_perm(len, 0, 0x0123);
   a.sizes[b] = (uint64_t)len + 4;
 }
 
-// ----------------------------------------------------------------- decoder
-struct Dec {
-  uint32_t low, range, code;
-  uint32_t cur;   // next input bytes, big-endian at the top
-  uint32_t avail; // bytes left in cur
-  uint32_t wi;    // index of the next word to load
-  uint32_t wlast; // last readable word (reads are clamped; overruns are detected by count)
-  uint32_t pulled;
-  const uint32_t* words;
-  __device__ __forceinline__ uint32_t next_byte() {
-    ++pulled;
-    if (avail == 0) {
-      cur = __byte_perm(__ldg(words + min(wi, wlast)), 0, 0x0123);
-      ++wi;
-      avail = 4;
-    }
-    const uint32_t b = cur >> 24;
-    cur <<= 8;
-    --avail;
-    return b;
-  }
-  __device__ __forceinline__ void step(uint32_t plo, uint32_t phi) {
-    low += plo;
-    range = phi - plo;
-    for (;;) {
-      const uint32_t t = low + range;
-      if (t < low || (low ^ t) >= kTop) {
-        if (range >= kBot) break;
-        range = (0u - low) & (kBot - 1u);
-      }
-      code = (code << 8) | next_byte();
-      low <<= 8;
-      range <<= 8;
-    }
-  }
-};
-
 template <int W>
-__device__ __forceinline__ uint32_t dec_symbol(Dec& d, SModel<W>& m, uint32_t unit) {
+__device__ __forceinline__ uint32_t dec_symbol(RcDec& d, SModel<W>& m, uint32_t unit) {
   // code < low only in a malformed stream; x = 0 then yields symbol 0 with
   // the same bounds the reference's search gives for a negative target
-  const uint32_t x = d.code >= d.low ? d.code - d.low : 0u;
+  const uint32_t x = d.offset();
   uint32_t plo, phi;
   const uint32_t s = m.find(x, unit, plo, phi);
-  d.step(plo, phi);
+  d.advance(plo, phi);
   m.add(s);
   return s;
 }
@@ -281,31 +211,14 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
     return;
   }
   const uint8_t* src = a.payload_in + o0;
-  uint32_t hdr = 0, code = 0;
+  uint32_t hdr = 0;
   for (int k = 0; k < 4; ++k) hdr = (hdr << 8) | src[k];
   if ((uint64_t)hdr + 4 != o1 - o0) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
-  for (int k = 4; k < 8; ++k) code = (code << 8) | src[k];
-  Dec d;
-  d.low = 0;
-  d.range = 0xFFFFFFFFu;
-  d.code = code;
-  d.pulled = 0;
-  {
-    // words are indexed from the aligned word holding src+4 (always inside the
-    // block); every load is clamped to the word holding the block's last byte
-    const uintptr_t base = reinterpret_cast<uintptr_t>(src + 4) & ~(uintptr_t)3;
-    const uintptr_t last = reinterpret_cast<uintptr_t>(a.payload_in + o1 - 1) & ~(uintptr_t)3;
-    const uint32_t off = (uint32_t)(reinterpret_cast<uintptr_t>(src + 8) - base);
-    d.words = reinterpret_cast<const uint32_t*>(base);
-    d.wlast = (uint32_t)((last - base) >> 2);
-    const uint32_t w0 = off >> 2, skip = off & 3;
-    d.cur = __byte_perm(__ldg(d.words + min(w0, d.wlast)), 0, 0x0123) << (8 * skip);
-    d.avail = 4 - skip;
-    d.wi = w0 + 1;
-  }
+  RcDec d;
+  d.init(src, a.payload_in + o1);
   SModel<W> m;
   m.init();
   uint8_t* dst = a.packed_out + st.byte_off[si] + start * W / 8;
@@ -346,7 +259,7 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   }
   // bytes consumed = 4 header + 4 priming + pulled; pulling past the block is
   // a truncated stream (codecs.py:283-288)
-  if ((uint64_t)d.pulled + 8 > o1 - o0) atomicOr(a.status, KVC_FLAG_CODEC);
+  if ((uint64_t)d.pulled() + 8 > o1 - o0) atomicOr(a.status, KVC_FLAG_CODEC);
 }
 
 }  // namespace
