@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libkvc.so")
-SOURCES = ["api.cu", "generic.cu", "fast128.cu", "uchan128.cu", "codec.cu", "rc_small.cu", "rc_large.cu", "rc_tables.cu", "delta128.cu", "profile.cpp"]
+SOURCES = ["api.cu", "generic.cu", "fast128.cu", "uchan128.cu", "codec.cu", "rc_small.cu", "rc_large.cu", "rc_tables.cu", "delta128.cu", "fused_rc.cu", "profile.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -339,6 +339,37 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
   if ((e = launch_setup(g, meta, st, heads, s)) != cudaSuccess) return cuda_fail(e, "setup");
   if (g.transform == T_AFFINE)
     if ((e = launch_affine_calibrate(g, kv, meta, s)) != cudaSuccess) return cuda_fail(e, "affine");
+  if (fused_rc_applicable(g)) {
+    // quantize + range code in one pass, then block offsets + gather
+    FusedArgs f;
+    memset(&f, 0, sizeof f);
+    f.g = g;
+    f.kv = kv;
+    f.scales = reinterpret_cast<__half*>(meta);
+    f.zeros = f.scales + g.ngroups;
+    f.slots = ws + p.ws_slots;
+    f.sizes = reinterpret_cast<uint64_t*>(ws + p.ws_sizes);
+    f.slot_bytes = p.slot_bytes;
+    f.max_blocks = p.max_blocks;
+    f.status = status;
+    for (int w = 1; w <= 8; ++w) f.rl[w] = 1.0f / (float)((1 << w) - 1);
+    if ((e = launch_fused_rc_encode(f, s)) != cudaSuccess) return cuda_fail(e, "fused encode");
+    CodecArgs c;
+    memset(&c, 0, sizeof c);
+    c.g = g;
+    c.st = st;
+    c.payload_out = reinterpret_cast<uint8_t*>(payload);
+    c.offsets = block_offsets;
+    c.slots = f.slots;
+    c.sizes = f.sizes;
+    c.scan_tmp = ws + p.ws_scan;
+    c.scan_bytes = (size_t)p.scan_bytes;
+    c.slot_bytes = p.slot_bytes;
+    c.max_blocks = p.max_blocks;
+    c.status = status;
+    if ((e = launch_codec_finish(c, s)) != cudaSuccess) return cuda_fail(e, "codec finish");
+    return KVC_OK;
+  }
   EncArgs a;
   memset(&a, 0, sizeof a);
   a.g = g;
@@ -399,6 +430,33 @@ static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payloa
   HeadEntry* heads = reinterpret_cast<HeadEntry*>(ws + p.ws_heads);
   cudaError_t e;
   if ((e = launch_setup(g, meta, st, heads, s)) != cudaSuccess) return cuda_fail(e, "setup");
+  if (fused_rc_applicable(g)) {
+    CodecArgs c;
+    memset(&c, 0, sizeof c);
+    c.g = g;
+    c.st = st;
+    c.offsets_in = block_offsets;
+    c.payload_bytes = payload_bytes;
+    c.status = status;
+    if ((e = launch_check_payload(c, s)) != cudaSuccess) return cuda_fail(e, "check payload");
+    FusedArgs f;
+    memset(&f, 0, sizeof f);
+    f.g = g;
+    f.scales_in = reinterpret_cast<const __half*>(meta);
+    f.zeros_in = f.scales_in + g.ngroups;
+    f.payload_in = reinterpret_cast<const uint8_t*>(payload);
+    f.offsets_in = block_offsets;
+    f.payload_bytes = payload_bytes;
+    f.max_blocks = p.max_blocks;
+    f.out = out;
+    f.paged = paged;
+    f.block_table = block_table;
+    f.page_tokens = page_tokens;
+    f.layer_stride = layer_stride;
+    f.status = status;
+    if ((e = launch_fused_rc_decode(f, s)) != cudaSuccess) return cuda_fail(e, "fused decode");
+    return KVC_OK;
+  }
   const uint8_t* packed = reinterpret_cast<const uint8_t*>(payload);
   CodecArgs c;
   memset(&c, 0, sizeof c);

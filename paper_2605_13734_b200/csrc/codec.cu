@@ -284,7 +284,12 @@ cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  return launch_codec_finish(a, s);
+}
+
+cudaError_t launch_codec_finish(const CodecArgs& a, cudaStream_t s) {
   size_t tmp = a.scan_bytes;
+  cudaError_t e;
   {
     ProfScope ps("offset_scan", s);
     e = cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.sizes, a.offsets, (int)(a.max_blocks + 1), s);
@@ -296,15 +301,18 @@ cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_
   return cudaGetLastError();
 }
 
+cudaError_t launch_check_payload(const CodecArgs& a, cudaStream_t s) {
+  ProfScope ps("check_payload", s);
+  k_check_payload<<<1, 1, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_codec_decode(const CodecArgs& args, int sm_count, cudaStream_t s) {
   (void)sm_count;
   CodecArgs a = args;
   if (a.g.codec == C_ENTROPY) a.recip = recip_tables(s);
-  {
-    ProfScope ps("check_payload", s);
-    k_check_payload<<<1, 1, 0, s>>>(a);
-  }
-  if (a.g.codec == C_NONE) return cudaGetLastError();
+  cudaError_t ce = launch_check_payload(a, s);
+  if (ce != cudaSuccess || a.g.codec == C_NONE) return ce;
   const unsigned grid = (unsigned)((a.max_blocks + 127) / 128 + 1);
   bool used[9];
   widths_used(a.g, used);

@@ -1,5 +1,6 @@
 // Kernel argument blocks and launcher declarations.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -58,7 +59,33 @@ struct CodecArgs {
   const uint32_t* recip;      // [9][2048] reciprocal tables (rc_tables.cuh)
 };
 
-__device__ __forceinline__ int64_t out_index(const DecArgs& a, int64_t lh, int64_t t, int64_t c) {
+// Fused quantize + range-code kernels (fused_rc.cu): one thread per codec
+// block reads bf16 KV and writes its range-coded block (encode), or decodes a
+// block straight to KV (decode); no packed-symbol round trip through HBM.
+struct FusedArgs {
+  Geo g;
+  const void* kv;              // encode input, (L,H,T,C) bf16
+  __half* scales;              // encode: metadata scales / zeros out
+  __half* zeros;
+  const __half* scales_in;     // decode: metadata in
+  const __half* zeros_in;
+  uint8_t* slots;              // encode: slot_bytes per block
+  uint64_t* sizes;             // encode: per block (max_blocks + 1)
+  int64_t slot_bytes, max_blocks;
+  const uint8_t* payload_in;   // decode
+  const uint64_t* offsets_in;
+  int64_t payload_bytes;
+  void* out;                   // decode output (contiguous or paged)
+  int paged;
+  const int32_t* block_table;
+  int64_t page_tokens, layer_stride;
+  uint32_t* status;
+  const uint32_t* recip;
+  float rl[9];
+};
+
+template <class A>
+__device__ __forceinline__ int64_t out_index(const A& a, int64_t lh, int64_t t, int64_t c) {
   if (!a.paged) return (lh * a.g.T + t) * a.g.C + c;
   const int64_t l = lh / a.g.H, h = lh - l * a.g.H;
   const int64_t page = a.block_table[t / a.page_tokens];
@@ -98,5 +125,13 @@ cudaError_t launch_rc_large_decode(const CodecArgs& a, int w, cudaStream_t s);
 size_t codec_scan_bytes(int64_t max_blocks);
 cudaError_t launch_codec_encode(const CodecArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s);
+// block offsets (exclusive scan of sizes) + gather of slots into the payload
+cudaError_t launch_codec_finish(const CodecArgs& a, cudaStream_t s);
+cudaError_t launch_check_payload(const CodecArgs& a, cudaStream_t s);
+
+// fused quantize + range code (fused_rc.cu)
+bool fused_rc_applicable(const Geo& g);
+cudaError_t launch_fused_rc_encode(const FusedArgs& a, cudaStream_t s);
+cudaError_t launch_fused_rc_decode(const FusedArgs& a, cudaStream_t s);
 
 }  // namespace kvc

@@ -18,9 +18,22 @@ namespace kvc {
 constexpr uint32_t kRcTop = 1u << 24;
 constexpr uint32_t kRcBot = 1u << 16;
 
-__device__ __forceinline__ uint32_t rc_settled_bytes(uint32_t low, uint32_t range) {
-  const uint32_t t = low + range;
-  return t < low ? 0u : (__clz(low ^ t) >> 3);
+__device__ __forceinline__ uint32_t rc_clz(uint32_t x) {  // x != 0
+  uint32_t r;
+  asm("bfind.shiftamt.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// 8 * (number of settled leading bytes): 0, 8, 16 or 24 (branch-free: the
+// compiler would otherwise branch around the bit scan)
+__device__ __forceinline__ uint32_t rc_settled_shift(uint32_t low, uint32_t range) {
+  uint32_t sh;
+  asm("{\n\t.reg .u32 t, x, c;\n\t.reg .pred p;\n\t"
+      "add.u32 t, %1, %2;\n\txor.b32 x, %1, t;\n\tbfind.shiftamt.u32 c, x;\n\tand.b32 c, c, 24;\n\t"
+      "setp.lt.u32 p, t, %1;\n\tselp.u32 %0, 0, c, p;\n\t}"
+      : "=r"(sh)
+      : "r"(low), "r"(range));
+  return sh;
 }
 
 // Encoder: output bytes accumulate in a 64-bit window (newest byte lowest)
@@ -38,10 +51,9 @@ struct RcEnc {
     nb = 0;
     out = o;
   }
-  // shift the top k <= 3 bytes of low out (codecs.py:261-263, k times)
-  __device__ __forceinline__ void put(uint32_t k) {
-    const uint32_t sh = 8u * k;
-    const uint32_t bytes = __funnelshift_l(low, 0u, sh);  // low >> (32 - sh), 0 for k = 0
+  // shift the top sh/8 <= 3 bytes of low out (codecs.py:261-263, once per byte)
+  __device__ __forceinline__ void put_sh(uint32_t sh) {
+    const uint32_t bytes = __funnelshift_l(low, 0u, sh);  // low >> (32 - sh), 0 for sh = 0
     whi = __funnelshift_l(wlo, whi, sh);
     wlo = (wlo << sh) | bytes;
     const uint32_t o = nb;
@@ -50,6 +62,7 @@ struct RcEnc {
     low <<= sh;
     range <<= sh;
   }
+  __device__ __forceinline__ void put(uint32_t k) { put_sh(8u * k); }
   __device__ __forceinline__ void underflow() {  // the reference's loop, from a settled state
     for (;;) {
       const uint32_t t = low + range;
@@ -63,8 +76,27 @@ struct RcEnc {
   __device__ __forceinline__ void encode(uint32_t unit, uint32_t cum, uint32_t freq) {
     low += unit * cum;
     range = unit * freq;
-    put(rc_settled_bytes(low, range));
+    put_sh(rc_settled_shift(low, range));
     if (range < kRcBot) underflow();
+  }
+  // Same, for lanes known to be converged (`mask`): the rare underflow loop
+  // runs warp-uniformly, each lane stepping the reference loop predicated on
+  // its own state, so the common path carries no divergent branch.
+  __device__ __forceinline__ void encode_warp(uint32_t unit, uint32_t cum, uint32_t freq, unsigned mask) {
+    low += unit * cum;
+    range = unit * freq;
+    put_sh(rc_settled_shift(low, range));
+    if (__any_sync(mask, range < kRcBot)) {
+      for (;;) {
+        const uint32_t t = low + range;
+        const bool differ = t < low || (low ^ t) >= kRcTop;
+        const bool fix = differ && range < kRcBot;
+        const bool emit = !differ || fix;
+        if (!__any_sync(mask, emit)) break;
+        if (fix) range = (0u - low) & (kRcBot - 1u);
+        put_sh(emit ? 8u : 0u);
+      }
+    }
   }
   // finish (codecs.py:266-270): four bytes of low, then the partial word;
   // returns the byte count
@@ -85,11 +117,13 @@ struct RcDec {
   uint32_t hi, lo;
   uint32_t avail;  // bytes in the window; >= 4 between symbols
   uint32_t wi, wlast, skip;
+  uint32_t nxt;  // word wi, loaded one refill ahead so its latency is hidden
   const uint32_t* words;
 
   __device__ __forceinline__ uint32_t load() {
-    const uint32_t w = __byte_perm(__ldg(words + min(wi, wlast)), 0, 0x0123);
+    const uint32_t w = __byte_perm(nxt, 0, 0x0123);
     ++wi;
+    nxt = __ldg(words + min(wi, wlast));
     return w;
   }
   __device__ __forceinline__ void refill() {
@@ -108,6 +142,7 @@ struct RcDec {
     wlast = (uint32_t)((last - base) >> 2);
     skip = (uint32_t)(reinterpret_cast<uintptr_t>(blk + 4) - base);  // 0..3
     wi = 0;
+    nxt = __ldg(words);
     hi = load() << (8u * skip);
     const uint32_t w1 = load();
     if (skip == 0) {
@@ -127,17 +162,17 @@ struct RcDec {
     low = 0;
     range = 0xFFFFFFFFu;
   }
-  // pull k <= 3 bytes into code (codecs.py:303-305, k times)
-  __device__ __forceinline__ void take(uint32_t k) {
-    const uint32_t sh = 8u * k;
+  // pull sh/8 <= 3 bytes into code (codecs.py:303-305, once per byte)
+  __device__ __forceinline__ void take_sh(uint32_t sh) {
     code = (code << sh) | __funnelshift_l(hi, 0u, sh);
     hi = __funnelshift_l(lo, hi, sh);
     lo <<= sh;
-    avail -= k;
+    avail -= sh >> 3;
     low <<= sh;
     range <<= sh;
     refill();
   }
+  __device__ __forceinline__ void take(uint32_t k) { take_sh(8u * k); }
   // stream bytes consumed after the 4 priming bytes
   __device__ __forceinline__ uint32_t pulled() const { return 4u * wi - skip - 4u - avail; }
   __device__ __forceinline__ void underflow() {
@@ -155,8 +190,25 @@ struct RcDec {
   __device__ __forceinline__ void advance(uint32_t plo, uint32_t phi) {  // plo = unit*cum, phi = unit*(cum+freq)
     low += plo;
     range = phi - plo;
-    take(rc_settled_bytes(low, range));
+    take_sh(rc_settled_shift(low, range));
     if (range < kRcBot) underflow();
+  }
+  // converged-lane variant (see RcEnc::encode_warp)
+  __device__ __forceinline__ void advance_warp(uint32_t plo, uint32_t phi, unsigned mask) {
+    low += plo;
+    range = phi - plo;
+    take_sh(rc_settled_shift(low, range));
+    if (__any_sync(mask, range < kRcBot)) {
+      for (;;) {
+        const uint32_t t = low + range;
+        const bool differ = t < low || (low ^ t) >= kRcTop;
+        const bool fix = differ && range < kRcBot;
+        const bool pull = !differ || fix;
+        if (!__any_sync(mask, pull)) break;
+        if (fix) range = (0u - low) & (kRcBot - 1u);
+        take_sh(pull ? 8u : 0u);
+      }
+    }
   }
 };
 

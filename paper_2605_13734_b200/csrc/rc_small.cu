@@ -21,86 +21,11 @@
 #include "kernels.h"
 #include "profile.h"
 #include "rc_coder.cuh"
+#include "rc_model.cuh"
 #include "rc_tables.cuh"
 
 namespace kvc {
 namespace {
-
-constexpr int kH = 2048;  // first halving after symbol kH-1 for every A in 2..16
-
-template <int W>
-struct SModel {
-  static constexpr int A = 1 << W;
-  uint32_t C[A];  // C[k] = sum of f[0..k-1] for k = 1..A-1 (C[0] unused)
-  uint32_t total;
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int k = 1; k < A; ++k) C[k] = k;
-    total = A;
-  }
-  __device__ __forceinline__ void lookup(uint32_t s, uint32_t& lo, uint32_t& hi) const {
-    lo = 0;
-    hi = C[1];
-#pragma unroll
-    for (int k = 1; k < A; ++k) {
-      const bool ge = s >= (uint32_t)k;
-      lo = ge ? C[k] : lo;
-      hi = ge ? (k + 1 < A ? C[k + 1] : total) : hi;
-    }
-  }
-  __device__ __forceinline__ void add(uint32_t s) {  // f[s] += 32 (codecs.py:227-230)
-#pragma unroll
-    for (int k = 1; k < A; ++k) C[k] += (s < (uint32_t)k) ? 32u : 0u;
-    total += 32u;
-  }
-  __device__ void halve() {  // codecs.py:234-242
-    uint32_t prev = 0, t = 0;
-#pragma unroll
-    for (int k = 1; k <= A; ++k) {
-      const uint32_t ck = (k == A) ? total : C[k];
-      uint32_t f = (ck - prev) >> 1;
-      f = f ? f : 1u;
-      prev = ck;
-      t += f;
-      if (k < A) C[k] = t;
-    }
-    total = t;
-  }
-  // decode: s with C[s] <= target = min(x / unit, total - 1); returns unit*C[s], unit*C[s+1]
-  __device__ __forceinline__ uint32_t find(uint32_t x, uint32_t unit, uint32_t& plo, uint32_t& phi) const {
-    if constexpr (A <= 4) {
-      // x >= unit*C[k]  <=>  floor(x / unit) >= C[k]; the clamp to total-1 never
-      // changes the symbol because C[A-1] <= total - 1
-      uint32_t s = 0;
-      plo = 0;
-      phi = unit * C[1];
-#pragma unroll
-      for (int k = 1; k < A; ++k) {
-        const uint32_t pk = unit * C[k];
-        const uint32_t pn = unit * (k + 1 < A ? C[k + 1] : total);
-        const bool ge = x >= pk;
-        s += ge ? 1u : 0u;
-        plo = ge ? pk : plo;
-        phi = ge ? pn : phi;
-      }
-      return s;
-    } else {
-      uint32_t target = x / unit;
-      target = target < total - 1 ? target : total - 1;
-      uint32_t s = 0, lo = 0, hi = C[1];
-#pragma unroll
-      for (int k = 1; k < A; ++k) {
-        const bool ge = target >= C[k];
-        s += ge ? 1u : 0u;
-        lo = ge ? C[k] : lo;
-        hi = ge ? (k + 1 < A ? C[k + 1] : total) : hi;
-      }
-      plo = unit * lo;
-      phi = unit * hi;
-      return s;
-    }
-  }
-};
 
 template <int W>
 __device__ __forceinline__ uint32_t sym_at(const uint32_t* wd, int j) {
@@ -184,18 +109,6 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
 }
 
 template <int W>
-__device__ __forceinline__ uint32_t dec_symbol(RcDec& d, SModel<W>& m, uint32_t unit) {
-  // code < low only in a malformed stream; x = 0 then yields symbol 0 with
-  // the same bounds the reference's search gives for a negative target
-  const uint32_t x = d.offset();
-  uint32_t plo, phi;
-  const uint32_t s = m.find(x, unit, plo, phi);
-  d.advance(plo, phi);
-  m.add(s);
-  return s;
-}
-
-template <int W>
 __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,7 +148,7 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
       const uint32_t unit = div_recip(d.range, m.total, mg[j]);
-      acc = (acc << W) | dec_symbol<W>(d, m, unit);
+      acc = (acc << W) | dec_symbol_small<W>(d, m, unit);
       nbits += W;
       if (nbits >= 32) {
         nbits -= 32;
@@ -249,7 +162,7 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   int nacc = 0, nout = i * W / 8;
   for (; i < n; ++i) {
     const uint32_t unit = (i < kH) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
-    acc = (acc << W) | dec_symbol<W>(d, m, unit);
+    acc = (acc << W) | dec_symbol_small<W>(d, m, unit);
     if (m.total >= 65536u) m.halve();
     nacc += W;
     while (nacc >= 8) {

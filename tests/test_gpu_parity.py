@@ -241,3 +241,59 @@ def test_f32_input_matches_reference_fixture():
         assert blob.metadata_bytes() == metas[k], sid
         out = codec.decode(blob).cpu().numpy()
         assert np.array_equal(out.view(np.uint32), g["recon"][k].view(np.uint32)), sid
+
+
+@pytest.mark.parametrize("q", ["uniform", "uchan"])
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+@pytest.mark.parametrize("block", [128, 512, 2048])
+def test_fused_entropy(q, b, block):
+    """Fused quantize + range-code kernels (fused_rc.cu): per-token groups with
+    a ragged last block, per-channel groups with several token chunks."""
+    sid = f"t=identity;q={q},b={b},g=32;c=entropy"
+    shape = (2, 2, 2048, 128) if q == "uchan" else (1, 3, 300, 128)
+    got, rec, _ = run_case(sid, shape, seed=b * 13 + block, block=block)
+    assert np.array_equal(got.view(np.uint32), rec.view(np.uint32)), sid
+
+
+@pytest.mark.parametrize("q", ["uniform", "uchan"])
+def test_fused_entropy_bf16_and_paged(q):
+    from paper_2605_13734_b200 import KVCodec
+
+    L, H, T, C = 2, 4, 1024, 128
+    v, _ = oracle.generate_kv(L, H, T, C, seed=21)
+    kv = torch.from_numpy(v).to(torch.bfloat16).cuda()
+    sid = f"t=identity;q={q},b=2,g=32;c=entropy"
+    ref = oracle.encode_blob(kv.float().cpu().numpy(), None, sid, block=512)
+    rec = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, (L, H, T, C), block=512)
+    codec = KVCodec(sid, (L, H, T, C), block_symbols=512)
+    blob = codec.encode(kv)
+    codec.check()
+    assert blob.payload_bytes() == ref["payload"]
+    flat = codec.decode(blob)
+    codec.check(decoding=True)
+    assert torch.equal(flat, torch.from_numpy(rec).to(torch.bfloat16).cuda())
+    P = 16
+    npages = T // P + 5
+    table = torch.randperm(npages, device="cuda")[: T // P].to(torch.int32)
+    pages = torch.zeros(L * npages * P * H * C, dtype=torch.bfloat16, device="cuda")
+    codec.decode_paged(blob, pages, table, P, npages * P * H * C)
+    codec.check(decoding=True)
+    pv = pages.view(L, npages, P, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
+    assert torch.equal(pv, flat)
+
+
+def test_fused_uchan_rejects_corruption():
+    from paper_2605_13734_b200 import KVCodec, _native
+
+    shape = (1, 2, 1024, 128)
+    v, _ = oracle.generate_kv(*shape, seed=3)
+    sid = "t=identity;q=uchan,b=2,g=32;c=entropy"
+    codec = KVCodec(sid, shape, block_symbols=512)
+    blob = codec.encode(torch.from_numpy(v).to(torch.bfloat16).cuda())
+    codec.check()
+    off = blob.offsets_array()
+    k = int(off[37])
+    blob.payload[k + 2] = blob.payload[k + 2] ^ 0x10  # block 37's length header
+    codec.decode(blob)
+    with pytest.raises(_native.CodecError):
+        codec.check(decoding=True)
