@@ -404,6 +404,9 @@ def main():
         alg.setdefault("rle_encode", []).append(packed + coded)
         alg.setdefault("rle_decode", []).append(packed + coded)
         alg.setdefault("gather", []).append(2 * coded)
+        # fused quantize + range code: bf16 in, coded blocks + metadata out (and the reverse)
+        alg.setdefault("fused_encode", []).append(2 * E + coded + meta)
+        alg.setdefault("fused_decode", []).append(2 * E + coded + meta)
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_n) = dom
     per_launch_ms = dom_ms / dom_n

@@ -70,17 +70,31 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <int W>
 __device__ __forceinline__ void pack32_store(const float* q, uint8_t* dst) {
   uint32_t be[W];
+  if constexpr (32 % W == 0) {
+    // whole symbols per word: an IMAD chain over the magic floats' bit
+    // patterns (kMagicBits + symbol), the constant part removed once per word
+    constexpr int per = 32 / W;
+    constexpr uint32_t fix = kMagicBits * (0xFFFFFFFFu / ((1u << W) - 1u));
 #pragma unroll
-  for (int k = 0; k < W; ++k) be[k] = 0;
+    for (int k = 0; k < W; ++k) {
+      uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const uint32_t s = __float_as_uint(q[i]) & ((1u << W) - 1u);
-    const int p = i * W, k = p >> 5, off = p & 31;
-    if (off + W <= 32) {
-      be[k] |= s << (32 - off - W);
-    } else {
-      be[k] |= s >> (off + W - 32);
-      be[k + 1] |= s << (64 - off - W);
+      for (int j = 0; j < per; ++j) acc += __float_as_uint(q[k * per + j]) * (1u << (32 - W * (j + 1)));
+      be[k] = acc - fix;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) be[k] = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t s = __float_as_uint(q[i]) & ((1u << W) - 1u);
+      const int p = i * W, k = p >> 5, off = p & 31;
+      if (off + W <= 32) {
+        be[k] |= s << (32 - off - W);
+      } else {
+        be[k] |= s >> (off + W - 32);
+        be[k + 1] |= s << (64 - off - W);
+      }
     }
   }
   uint32_t wd[W];
@@ -246,7 +260,24 @@ __device__ __forceinline__ void quantize64(float* y, float mn0, float mx0, float
         zeros[gi] = z16;
       }
       float* yy = y + c * 32;
+      // no clip needed when the exact quotients of the group's min and max
+      // already round into [0, levels] (monotone in v); decided per warp
+      bool easy = false;
       if (q.mode == 0) {
+        const float dl = __fsub_rn(gmn[c], q.z), dh = __fsub_rn(gmx[c], q.z);
+        const float l0 = __fmul_rn(dl, q.r), h0 = __fmul_rn(dh, q.r);
+        const float l1 = __fmaf_rn(__fmaf_rn(-l0, q.s, dl), q.r, l0);
+        const float h1 = __fmaf_rn(__fmaf_rn(-h0, q.s, dh), q.r, h0);
+        easy = l1 >= -0.5f && h1 < q.lv + 0.5f;
+      }
+      if (__all_sync(0xffffffffu, easy)) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float d = __fsub_rn(yy[i], q.z);
+          const float q0 = __fmul_rn(d, q.r);
+          yy[i] = __fadd_rn(__fmaf_rn(__fmaf_rn(-q0, q.s, d), q.r, q0), kMagicRound);
+        }
+      } else if (q.mode == 0) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) yy[i] = quant_magic(yy[i], q);
       } else {

@@ -63,16 +63,18 @@ static __device__ __noinline__ float hadamard_slow(double Sp, double hc, uint32_
   return y;
 }
 
-// Branch-free fast path: RN64(S * RN64(1/c)) rounded to f32 with integer
-// ops.  `slow` is set when the result must come from hadamard_slow: the
-// magnitude is outside [2^-126, 2^128) or within 4 ulp64 of a midpoint.
+// Branch-free fast path: q = RN64(S * RN64(1/c)), rounded to f32 by the
+// hardware conversion (one F2F.F32.F64; its pipe has room in this issue-bound
+// kernel).  q can differ from the reference's RN64(S / c) by one ulp64, which
+// changes the f32 result only next to an f32 rounding boundary: `slow` is set
+// when q lies within 4 ulp64 of a midpoint or outside the normal f32 range
+// [2^-126, 2^128) (where the boundaries sit elsewhere), and the caller then
+// takes hadamard_slow.
 __device__ __forceinline__ float hadamard_fast(double Sp, double hk, bool& slow) {
   const double q = Sp * hk;
   const uint32_t H = (uint32_t)__double2hiint(q), Lw = (uint32_t)__double2loint(q);
-  const uint32_t m = Lw & 0x1FFFFFFFu;
-  slow = ((H & 0x7FFFFFFFu) - 0x38100000u >= 0x0FE00000u) | ((m - 0x0FFFFFFCu) <= 8u);
-  const uint32_t t = __funnelshift_l(Lw, H, 3) - 0xC0000000u + (m > 0x10000000u ? 1u : 0u);
-  return __uint_as_float((t & 0x7FFFFFFFu) | (H & 0x80000000u));
+  slow = ((H & 0x7FFFFFFFu) - 0x38100000u >= 0x0FE00000u) | (((Lw & 0x1FFFFFFFu) - 0x0FFFFFFCu) <= 8u);
+  return __double2float_rn(q);
 }
 
 __device__ __forceinline__ float hadamard_out(double Sp, double hk, double hc, uint32_t& flags) {
