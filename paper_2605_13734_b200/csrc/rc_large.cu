@@ -97,6 +97,24 @@ struct LModel {
       if (p <= (uint32_t)A) set(p, T(p) + T(j));
     }
   }
+  // Decoder search without the division: the largest s with
+  // unit * prefix(s) <= x, which is find(min(x // unit, total - 1))
+  // (codecs.py:214-225, :290-292) since a <= x // unit <=> a * unit <= x and
+  // prefix(A-1) <= total - 1; plo = unit * prefix(s).  No overflow: partial
+  // sums stay <= unit * total <= range.
+  __device__ __forceinline__ uint32_t find_scaled(uint32_t x, uint32_t unit, uint32_t& plo) const {
+    uint32_t pos = 0, acc = 0;
+#pragma unroll
+    for (uint32_t bit = A / 2; bit; bit >>= 1) {
+      const uint32_t v = acc + unit * T(pos + bit);
+      if (v <= x) {
+        acc = v;
+        pos += bit;
+      }
+    }
+    plo = acc;
+    return pos;
+  }
   // largest s with prefix(s) <= target (codecs.py:214-225); cum = prefix(s)
   __device__ __forceinline__ uint32_t find(uint32_t target, uint32_t& cum) const {
     uint32_t pos = 0, rem = target;
@@ -191,17 +209,11 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   int nacc = 0, nout = 0;
   for (int i = 0; i < n; ++i) {
     const uint32_t unit = (i < H) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
-    uint32_t s, cum;
-    if (d.code >= d.low) {
-      uint32_t target = (d.code - d.low) / unit;
-      target = target < m.total - 1 ? target : m.total - 1;
-      s = m.find(target, cum);
-    } else {  // malformed stream: the reference's search yields symbol 0
-      s = 0;
-      cum = 0;
-    }
+    // code < low only in a malformed stream; offset() reads 0 -> symbol 0
+    uint32_t plo;
+    const uint32_t s = m.find_scaled(d.offset(), unit, plo);
     const uint32_t fr = m.freq(s);
-    d.advance(unit * cum, unit * (cum + fr));
+    d.advance(plo, plo + unit * fr);
     m.bump(s);
     acc = (acc << W) | s;
     nacc += W;
@@ -212,6 +224,208 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   }
   // bytes consumed = 4 header + 4 priming + pulled (codecs.py:283-288)
   if ((int64_t)d.pulled() + 8 > len) atomicOr(a.status, KVC_FLAG_CODEC);
+}
+
+// ------------------------------------------------ two-phase encoder
+// The model values the coder needs at position i (cum, freq, total) depend
+// only on the block's symbols, not on the coder state, so for blocks of at
+// most 2048 symbols they are computed first, a warp per block, and the coder
+// threads then run on precomputed (cum << 16 | freq) words:
+//   before the first halving (i < H): f[v] = 1 + 32 c_v(i), so
+//     cum_i = s + 32 * #{j < i : s_j < s},  freq_i = 1 + 32 * #{j < i : s_j = s}
+//   (codecs.py:188-242).  The warp takes 32 positions at a time: counts over
+//   earlier chunks come from a shared prefix-count array P, counts among
+//   earlier lanes of the chunk from a radix ballot rank.
+//   at the halving (after position H-1) f'[v] = max(1, f[v] // 2) =
+//   (c_v ? 16 c_v : 1), so the <= 2048 - H tail positions use
+//   cum' = 16 P[s] + #{v < s : c_v = 0} plus 32 per earlier smaller tail
+//   symbol, and total' = 16 H + #{v : c_v = 0} (+ 32 per tail position).
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// rank of each valid lane's W-bit symbol among the earlier valid lanes:
+// less = #{earlier lanes with a smaller symbol}, returns the mask of earlier
+// lanes with an equal symbol
+template <int W>
+__device__ __forceinline__ unsigned ballot_rank(uint32_t s, unsigned earlier, uint32_t& less) {
+  unsigned eq = earlier;
+  less = 0;
+#pragma unroll
+  for (int bit = W - 1; bit >= 0; --bit) {
+    const bool one = (s >> bit) & 1u;
+    const unsigned bb = __ballot_sync(0xffffffffu, one);
+    if (one) {
+      less += __popc(eq & ~bb);
+      eq &= bb;
+    } else {
+      eq &= ~bb;
+    }
+  }
+  return eq;
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) k_rc_large_model(CodecArgs a, int64_t b0, int64_t nb) {
+  constexpr int A = 1 << W;
+  constexpr int H = halving_at<W>();
+  constexpr int K = A / 32;  // counters per lane
+  __shared__ __align__(16) uint32_t sP[4][A + 4];
+  __shared__ __align__(16) uint32_t sH[4][A + 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bl = (int64_t)blockIdx.x * 4 + warp;
+  if (bl >= nb) return;  // whole warp
+  const int64_t b = b0 + bl;
+  const StreamTab& st = *a.st;
+  if (b >= st.nblocks) return;
+  const int si = (st.n > 1 && b >= st.first_block[1]) ? 1 : 0;
+  if (st.w[si] != W) return;
+  const int64_t start = (b - st.first_block[si]) * a.g.block;
+  const int n = (int)min(a.g.block, st.count[si] - start);
+  const uint8_t* src = a.packed_in + st.byte_off[si] + start * W / 8;
+  uint32_t* P = sP[warp];
+  uint32_t* h = sH[warp];
+  for (int v = lane; v <= A; v += 32) P[v] = 0;
+  for (int v = lane; v < A; v += 32) h[v] = 0;
+  __syncwarp();
+  uint32_t* out = a.model + bl * a.g.block;
+  const unsigned lt = lanemask_lt();
+  const int nh = min(n, H);
+  auto sym_at = [&](int i) -> uint32_t {
+    if constexpr (W == 8) {
+      return src[i];
+    } else {
+      const int64_t p = (int64_t)i * W;
+      const uint32_t two = ((uint32_t)src[p >> 3] << 8) | src[(p >> 3) + 1];
+      return (two >> (16 - (int)(p & 7) - W)) & (A - 1);
+    }
+  };
+  for (int c0 = 0; c0 < nh; c0 += 32) {
+    const int i = c0 + lane;
+    const bool valid = i < nh;
+    const uint32_t s = valid ? sym_at(i) : 0u;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    uint32_t less;
+    const unsigned eq = ballot_rank<W>(s, lt & vmask, less);
+    const uint32_t ps = P[s], cs = P[s + 1] - ps;
+    if (valid) {
+      out[i] = ((s + 32u * (ps + less)) << 16) | (1u + 32u * (cs + __popc(eq)));
+      atomicAdd(&h[s], 1u);
+    }
+    __syncwarp();
+    // P[u + 1] += #{chunk symbols <= u}: lane-local inclusive prefix + warp scan
+    uint32_t cnt[K], run = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      run += h[lane * K + k];
+      cnt[k] = run;
+    }
+    uint32_t base = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, base, o);
+      if (lane >= o) base += t;
+    }
+    base -= run;  // exclusive
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      P[lane * K + k + 1] += base + cnt[k];
+      h[lane * K + k] = 0;
+    }
+    __syncwarp();
+  }
+  if (n > H) {
+    // the halved model (see above); h[v] <- #{u < v : c_u = 0}
+    uint32_t z[K], run = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int v = lane * K + k;
+      z[k] = run;
+      run += (P[v + 1] == P[v]) ? 1u : 0u;
+    }
+    uint32_t base = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, base, o);
+      if (lane >= o) base += t;
+    }
+    const uint32_t zeros_total = __shfl_sync(0xffffffffu, base, 31);
+    base -= run;
+#pragma unroll
+    for (int k = 0; k < K; ++k) h[lane * K + k] = base + z[k];
+    __syncwarp();
+    for (int c0 = H; c0 < n; c0 += 32) {  // one pass for block <= 2048
+      const int i = c0 + lane;
+      const bool valid = i < n;
+      const uint32_t s = valid ? sym_at(i) : 0u;
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      uint32_t less;
+      const unsigned eq = ballot_rank<W>(s, lt & vmask, less);
+      const uint32_t cs = P[s + 1] - P[s];
+      const uint32_t f1 = cs ? 16u * cs : 1u;
+      if (valid) out[i] = ((16u * P[s] + h[s] + 32u * less) << 16) | (f1 + 32u * __popc(eq));
+    }
+    if (lane == 0) a.model_total[bl] = 16u * (uint32_t)H + zeros_total;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) k_rc_large_code(CodecArgs a, int64_t b0, int64_t nb) {
+  constexpr int A = 1 << W;
+  constexpr int H = halving_at<W>();
+  const uint32_t* __restrict__ magic = a.recip + W * kRecipLen;
+  const int64_t bl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bl >= nb) return;
+  const int64_t b = b0 + bl;
+  if (b > a.max_blocks) return;
+  const StreamTab& st = *a.st;
+  if (b >= st.nblocks) {
+    a.sizes[b] = 0;
+    return;
+  }
+  const int si = (st.n > 1 && b >= st.first_block[1]) ? 1 : 0;
+  if (st.w[si] != W) return;
+  const int64_t start = (b - st.first_block[si]) * a.g.block;
+  const int n = (int)min(a.g.block, st.count[si] - start);
+  const uint4* mv = reinterpret_cast<const uint4*>(a.model + bl * a.g.block);
+  uint8_t* slot = a.slots + b * a.slot_bytes;
+  RcEnc e;
+  e.init(reinterpret_cast<uint32_t*>(slot + 4));
+  const uint32_t tail_total = n > H ? a.model_total[bl] : 0u;
+  const int nh = min(n, H) & ~3;  // whole quads before the halving: warp-converged fast loop
+  for (int i4 = 0; i4 < nh; i4 += 4) {
+    const unsigned mask = __activemask();
+    const uint4 q = __ldg(mv + (i4 >> 2));
+    const uint32_t qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t i = (uint32_t)(i4 + j);
+      const uint32_t unit = div_recip(e.range, (uint32_t)A + 32u * i, __ldg(magic + i));
+      e.encode_warp(unit, qv[j] >> 16, qv[j] & 0xFFFFu, mask);
+    }
+  }
+  for (int i = nh; i < n; ++i) {  // the rest (and the tail after the halving)
+    const uint32_t v = __ldg(a.model + bl * a.g.block + i);
+    const uint32_t unit = i < H ? div_recip(e.range, (uint32_t)A + 32u * (uint32_t)i, __ldg(magic + i))
+                                : e.range / (tail_total + 32u * (uint32_t)(i - H));
+    e.encode(unit, v >> 16, v & 0xFFFFu);
+  }
+  const uint32_t len = e.finish();
+  *reinterpret_cast<uint32_t*>(slot) = __byte_perm(len, 0, 0x0123);
+  a.sizes[b] = (uint64_t)len + 4;
+}
+
+template <int W>
+cudaError_t enc2_w(const CodecArgs& a, cudaStream_t s) {
+  const int64_t total = a.max_blocks + 1;  // block ids 0 .. max_blocks
+  for (int64_t b0 = 0; b0 < total; b0 += a.model_blocks) {
+    const int64_t nb = min(a.model_blocks, total - b0);
+    k_rc_large_model<W><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(a, b0, nb);
+    k_rc_large_code<W><<<(unsigned)((nb + 127) / 128), 128, 0, s>>>(a, b0, nb);
+  }
+  return cudaGetLastError();
 }
 
 template <int W>
@@ -241,6 +455,14 @@ cudaError_t dec_w(const CodecArgs& a, cudaStream_t s) {
 
 cudaError_t launch_rc_large_encode(const CodecArgs& a, int w, cudaStream_t s) {
   ProfScope ps("rc_encode", s);
+  if (a.model_blocks > 0 && a.g.block <= 2048) {
+    switch (w) {
+      case 5: return enc2_w<5>(a, s);
+      case 6: return enc2_w<6>(a, s);
+      case 7: return enc2_w<7>(a, s);
+      default: return enc2_w<8>(a, s);
+    }
+  }
   switch (w) {
     case 5: return enc_w<5>(a, s);
     case 6: return enc_w<6>(a, s);
