@@ -227,6 +227,43 @@ __device__ __forceinline__ void stage_value(uint8_t* tile, int row, int col, int
 }
 
 // ------------------------------------------------------------- per token
+// one block's groups; FULL = every lane of the warp codes a full block (the
+// warp-uniform votes then use a constant mask, with no divergence checks)
+template <int W, bool FULL>
+__device__ __forceinline__ void tok_encode_groups(const FusedArgs& a, const uint4* src, int64_t r0, int ngr, RcEnc& e,
+                                                  SModel<W>& m, uint32_t& flags, bool& nonfinite) {
+  const float rl = a.rl[W];
+  uint64_t sacc = 0, zacc = 0;
+#pragma unroll 1
+  for (int gi = 0; gi < ngr; ++gi) {
+    const unsigned mask = FULL ? 0xffffffffu : __activemask();
+    uint32_t wv[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 v = __ldg(src + gi * 4 + k);
+      wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
+    }
+    if (gi + 1 < ngr) {  // next group's 64 bytes
+      prefetch_l1(src + gi * 4 + 4);
+      prefetch_l1(src + gi * 4 + 6);
+    }
+    float mn, mx;
+    minmax_words(wv, mn, mx);
+    nonfinite |= isnan(mn);
+    __half s16, z16;
+    uint32_t nib[4];
+    quant32([&](int i) { return (i & 1) ? bf16_hi(wv[i >> 1]) : bf16_lo(wv[i >> 1]); }, mn, mx, W, rl, s16, z16, flags,
+            nib, mask);
+    sacc = (sacc >> 16) | ((uint64_t)__half_as_ushort(s16) << 48);
+    zacc = (zacc >> 16) | ((uint64_t)__half_as_ushort(z16) << 48);
+    if ((gi & 3) == 3) {  // a row's four groups: scales[row*4 .. +3]
+      *reinterpret_cast<uint64_t*>(a.scales + r0 * 4 + gi - 3) = sacc;
+      *reinterpret_cast<uint64_t*>(a.zeros + r0 * 4 + gi - 3) = zacc;
+    }
+    encode32<W>(e, m, gi * 32, nib, mask);
+  }
+}
+
 template <int W>
 __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedArgs a) {
   const Geo& g = a.g;
@@ -247,39 +284,16 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedAr
   e.init(reinterpret_cast<uint32_t*>(slot + 4));
   SModel<W> m;
   m.init();
-  const float rl = a.rl[W];
   uint32_t flags = 0;
   bool nonfinite = false;
-  const int ngr = nr * 4;
-  uint64_t sacc = 0, zacc = 0;
-#pragma unroll 1
-  for (int gi = 0; gi < ngr; ++gi) {
-    uint32_t wv[16];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint4 v = __ldg(src + gi * 4 + k);
-      wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
-    }
-    if (gi + 1 < ngr) {  // next group's 64 bytes
-      prefetch_l1(src + gi * 4 + 4);
-      prefetch_l1(src + gi * 4 + 6);
-    }
-    float mn, mx;
-    minmax_words(wv, mn, mx);
-    nonfinite |= isnan(mn);
-    __half s16, z16;
-    uint32_t nib[4];
-    const unsigned mask = __activemask();  // the ragged last block's warp may have exited lanes
-    quant32([&](int i) { return (i & 1) ? bf16_hi(wv[i >> 1]) : bf16_lo(wv[i >> 1]); }, mn, mx, W, rl, s16, z16, flags,
-            nib, mask);
-    sacc = (sacc >> 16) | ((uint64_t)__half_as_ushort(s16) << 48);
-    zacc = (zacc >> 16) | ((uint64_t)__half_as_ushort(z16) << 48);
-    if ((gi & 3) == 3) {  // a row's four groups: scales[row*4 .. +3]
-      *reinterpret_cast<uint64_t*>(a.scales + r0 * 4 + gi - 3) = sacc;
-      *reinterpret_cast<uint64_t*>(a.zeros + r0 * 4 + gi - 3) = zacc;
-    }
-    encode32<W>(e, m, gi * 32, nib, mask);
-  }
+  // only the warp holding the ragged last block (or lanes past the end) runs
+  // the activemask variant
+  const int64_t wlast = b - (threadIdx.x & 31) + 31;
+  const bool full = wlast < nblocks - 1 || (wlast == nblocks - 1 && nrows % R == 0);
+  if (full)
+    tok_encode_groups<W, true>(a, src, r0, nr * 4, e, m, flags, nonfinite);
+  else
+    tok_encode_groups<W, false>(a, src, r0, nr * 4, e, m, flags, nonfinite);
   const uint32_t len = e.finish();
   *reinterpret_cast<uint32_t*>(slot) = __byte_perm(len, 0, 0x0123);
   a.sizes[b] = (uint64_t)len + 4;

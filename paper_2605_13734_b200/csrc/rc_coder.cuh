@@ -63,6 +63,21 @@ struct RcEnc {
     range <<= sh;
   }
   __device__ __forceinline__ void put(uint32_t k) { put_sh(8u * k); }
+  // put_sh with the shifts done as multiplies by p = 2^sh: on the FMA pipe,
+  // off the saturated ALU pipe (low * p yields the shifted low and the
+  // outgoing bytes in one IMAD.WIDE)
+  __device__ __forceinline__ void put_mul(uint32_t sh) {
+    uint32_t p;
+    asm("shl.b32 %0, 1, %1;" : "=r"(p) : "r"(sh));  // opaque: keep the multiplies
+    const uint64_t lw = (uint64_t)low * p;
+    whi = __funnelshift_l(wlo, whi, sh);
+    wlo = wlo * p + (uint32_t)(lw >> 32);
+    low = (uint32_t)lw;
+    range *= p;
+    const uint32_t o = nb;
+    nb += sh;
+    if ((nb ^ o) >= 32u) out[(nb >> 5) - 1] = __byte_perm(__funnelshift_r(wlo, whi, nb), 0, 0x0123);
+  }
   __device__ __forceinline__ void underflow() {  // the reference's loop, from a settled state
     for (;;) {
       const uint32_t t = low + range;
@@ -85,7 +100,7 @@ struct RcEnc {
   __device__ __forceinline__ void encode_warp(uint32_t unit, uint32_t cum, uint32_t freq, unsigned mask) {
     low += unit * cum;
     range = unit * freq;
-    put_sh(rc_settled_shift(low, range));
+    put_mul(rc_settled_shift(low, range));
     if (__any_sync(mask, range < kRcBot)) {
       for (;;) {
         const uint32_t t = low + range;
