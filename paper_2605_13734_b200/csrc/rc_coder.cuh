@@ -188,6 +188,21 @@ struct RcDec {
     refill();
   }
   __device__ __forceinline__ void take(uint32_t k) { take_sh(8u * k); }
+  // take_sh with the shifts as multiplies by p = 2^sh (FMA pipe; see
+  // RcEnc::put_mul): hi * p yields the shifted window word and the bytes
+  // entering `code` in one IMAD.WIDE
+  __device__ __forceinline__ void take_mul(uint32_t sh) {
+    uint32_t p;
+    asm("shl.b32 %0, 1, %1;" : "=r"(p) : "r"(sh));
+    const uint64_t hw = (uint64_t)hi * p, lw = (uint64_t)lo * p;
+    code = code * p + (uint32_t)(hw >> 32);
+    hi = (uint32_t)hw + (uint32_t)(lw >> 32);
+    lo = (uint32_t)lw;
+    avail -= sh >> 3;
+    low *= p;
+    range *= p;
+    refill();
+  }
   // stream bytes consumed after the 4 priming bytes
   __device__ __forceinline__ uint32_t pulled() const { return 4u * wi - skip - 4u - avail; }
   __device__ __forceinline__ void underflow() {
@@ -212,7 +227,7 @@ struct RcDec {
   __device__ __forceinline__ void advance_warp(uint32_t plo, uint32_t phi, unsigned mask) {
     low += plo;
     range = phi - plo;
-    take_sh(rc_settled_shift(low, range));
+    take_mul(rc_settled_shift(low, range));
     if (__any_sync(mask, range < kRcBot)) {
       for (;;) {
         const uint32_t t = low + range;
