@@ -212,26 +212,43 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
 // blocks), the aligned body as 32-bit words funnel-shifted out of the
 // 16-byte-aligned slot
 __global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
   const StreamTab& st = *a.st;
-  if (b >= st.nblocks) return;
-  const uint64_t o0 = a.offsets[b], o1 = a.offsets[b + 1];
-  const uint32_t len = (uint32_t)(o1 - o0);
-  const uint8_t* src = a.slots + b * a.slot_bytes;
-  uint8_t* dst = a.payload_out + o0;
-  const uint32_t head = min((uint32_t)((4u - (uint32_t)(o0 & 3u)) & 3u), len);
-  const uint32_t words = (len - head) >> 2;
-  const uint32_t tail = len - head - 4 * words;
-  if (lane < (int)head) dst[lane] = src[lane];
-  if (lane < (int)tail) dst[head + 4 * words + lane] = src[head + 4 * words + lane];
-  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
-  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
-  const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
-  for (uint32_t w = lane; w < words; w += 32) {
-    const uint32_t lo = s32[w];
-    const uint32_t v = sh ? __funnelshift_r(lo, s32[w + 1], sh) : lo;
-    d32[w] = v;
+  const int64_t nb = st.nblocks;
+  // grid-stride over blocks; the next block's offsets are loaded while the
+  // current one is copied
+  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint64_t o0 = 0, o1 = 0;
+  if (b < nb) {
+    o0 = a.offsets[b];
+    o1 = a.offsets[b + 1];
+  }
+  for (; b < nb; b += nwarps) {
+    const int64_t bn = b + nwarps;
+    uint64_t n0 = 0, n1 = 0;
+    if (bn < nb) {
+      n0 = a.offsets[bn];
+      n1 = a.offsets[bn + 1];
+    }
+    const uint32_t len = (uint32_t)(o1 - o0);
+    const uint8_t* src = a.slots + b * a.slot_bytes;
+    uint8_t* dst = a.payload_out + o0;
+    const uint32_t head = min((uint32_t)((4u - (uint32_t)(o0 & 3u)) & 3u), len);
+    const uint32_t words = (len - head) >> 2;
+    const uint32_t tail = len - head - 4 * words;
+    if (lane < (int)head) dst[lane] = src[lane];
+    if (lane < (int)tail) dst[head + 4 * words + lane] = src[head + 4 * words + lane];
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+    const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
+    for (uint32_t w = lane; w < words; w += 32) {
+      const uint32_t lo = s32[w];
+      const uint32_t v = sh ? __funnelshift_r(lo, s32[w + 1], sh) : lo;
+      d32[w] = v;
+    }
+    o0 = n0;
+    o1 = n1;
   }
 }
 
@@ -295,7 +312,12 @@ cudaError_t launch_codec_finish(const CodecArgs& a, cudaStream_t s) {
     e = cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.sizes, a.offsets, (int)(a.max_blocks + 1), s);
   }
   if (e != cudaSuccess) return e;
-  const unsigned ggrid = (unsigned)((a.max_blocks * 32 + 255) / 256 + 1);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (a.max_blocks * 32 + 255) / 256 + 1;
+  const int64_t cap = (int64_t)sms * 16;  // 16 CTAs of 8 warps per SM, grid-stride beyond
+  const unsigned ggrid = (unsigned)(want < cap ? want : cap);
   ProfScope ps("gather", s);
   k_gather<<<ggrid, 256, 0, s>>>(a);
   return cudaGetLastError();

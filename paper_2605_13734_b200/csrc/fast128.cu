@@ -542,6 +542,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
     const int cb0 = had ? 32 * half : 64 * half;
     const int cb1 = had ? 64 + 32 * half : 64 * half + 32;
     const uint8_t* src = a.packed + (bit >> 3);
+    if constexpr (W != 0) {
+      // uniform width: the next tile's packed half-row and scales are at a
+      // fixed stride; pull them into L1 while this tile computes
+      const int64_t nrow = row + (int64_t)gridDim.x * kRows;
+      if (nrow < nrows) {
+        const uint8_t* np = src + (nrow - row) * 128 * W / 8;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(np + cb0 * W / 8));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(np + cb1 * W / 8));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(scales + nrow * (128 / G)));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(zeros + nrow * (128 / G)));
+      }
+    }
     float y[64];
     if constexpr (W == 0) {
       unpack32_dispatch(w, src + cb0 * w / 8, y);
