@@ -117,6 +117,27 @@ int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_
 const char* kvc_last_error(void);
 const char* kvc_version(void);
 
+/* Per-block CRC-32 (IEEE 802.3 / zlib.crc32 polynomial, reflected, init and
+ * final xor 0xFFFFFFFF) of an encoded payload: block b covers device bytes
+ * [block_offsets[b], block_offsets[b+1]) of `payload`; `crc` (device,
+ * nblocks entries) receives one checksum per block.  Used by the block-framed
+ * wire container (the reference blob has no checksum,
+ * codecs.py:41-59).  A whole-buffer checksum is nblocks = 1 with offsets
+ * {0, len}. */
+int kvc_block_crc32(const void* payload, const uint64_t* block_offsets, int64_t nblocks, uint32_t* crc, void* stream);
+
+/* Copy a data-dependent number of bytes without a host round trip: copies
+ * min(*nbytes_dev, max_bytes) bytes from src to dst, where *nbytes_dev is a
+ * device-resident length (e.g. block_offsets[nblocks] of an encode).  src and
+ * dst may live on different GPUs (peer access enabled with
+ * kvc_enable_peer_access): the kernel runs on the stream's device and moves
+ * 16-byte vectors over NVLink.  Used by the pipelined compress -> transfer ->
+ * decompress path. */
+int kvc_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes, void* stream);
+
+/* cudaDeviceEnablePeerAccess(peer) from `device` (already-enabled is OK). */
+int kvc_enable_peer_access(int device, int peer);
+
 /* Per-kernel timing (the native side of the StageTimer hook, compress.py:43-48).
  * When enabled, every kernel the library launches on the calling thread is
  * bracketed by CUDA events on its stream.  kvc_profile_collect synchronises,

@@ -39,6 +39,9 @@ EXPORTS = (
     "kvc_version",
     "kvc_profile_enable",
     "kvc_profile_collect",
+    "kvc_block_crc32",
+    "kvc_copy_device_length",
+    "kvc_enable_peer_access",
 )
 
 
@@ -99,6 +102,12 @@ def lib() -> ctypes.CDLL:
     L.kvc_profile_enable.restype = I32
     L.kvc_profile_collect.argtypes = [ctypes.c_char_p, I64, P, P, I32]
     L.kvc_profile_collect.restype = I32
+    L.kvc_block_crc32.argtypes = [P, P, I64, P, P]
+    L.kvc_block_crc32.restype = I32
+    L.kvc_copy_device_length.argtypes = [P, P, P, I64, P]
+    L.kvc_copy_device_length.restype = I32
+    L.kvc_enable_peer_access.argtypes = [I32, I32]
+    L.kvc_enable_peer_access.restype = I32
     _lib = L
     return L
 

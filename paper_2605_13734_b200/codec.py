@@ -104,6 +104,7 @@ class KVCodec:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.in_dtype = in_dtype
         self.out_dtype = out_dtype
+        self.block_symbols = int(block_symbols)
         opts = N.KvcOptions()
         opts.block_symbols = int(block_symbols)
         opts.in_dtype = N.DTYPE_BF16 if in_dtype == torch.bfloat16 else N.DTYPE_F32

@@ -523,6 +523,43 @@ int kvc_decode_paged(const kvc_plan* plan, const void* payload, int64_t payload_
                      layer_stride, workspace, stream);
 }
 
+int kvc_block_crc32(const void* payload, const uint64_t* block_offsets, int64_t nblocks, uint32_t* crc, void* stream) {
+  if (nblocks < 0) return fail(KVC_ERR_CONFIG, "nblocks < 0");
+  if (nblocks == 0) return KVC_OK;
+  if (!payload || !block_offsets || !crc) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  cudaError_t e = launch_block_crc32(reinterpret_cast<const uint8_t*>(payload), block_offsets, nblocks, crc,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "block crc32");
+  return KVC_OK;
+}
+
+int kvc_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes, void* stream) {
+  if (max_bytes <= 0) return KVC_OK;
+  if (!dst || !src || !nbytes_dev) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  cudaError_t e = launch_copy_device_length(dst, src, nbytes_dev, max_bytes, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "copy");
+  return KVC_OK;
+}
+
+int kvc_enable_peer_access(int device, int peer) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (device == peer) return KVC_OK;
+  int can = 0;
+  cudaError_t e = cudaDeviceCanAccessPeer(&can, device, peer);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceCanAccessPeer");
+  if (!can) return fail(KVC_ERR_CONFIG, "no peer access between these devices");
+  cudaSetDevice(device);
+  e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(cur);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return KVC_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return KVC_OK;
+}
+
 int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_t* flags) {
   if (!plan || !workspace || !flags) return fail(KVC_ERR_CONFIG, "NULL argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

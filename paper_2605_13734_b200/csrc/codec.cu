@@ -351,4 +351,87 @@ cudaError_t launch_codec_decode(const CodecArgs& args, int sm_count, cudaStream_
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ block CRC-32
+// One thread per block, slicing-by-4 over 32-bit words with the four 256-entry
+// tables in shared memory (built per CTA); unaligned head / tail bytes one at
+// a time.  Blocks are a few hundred bytes, so this is a small fraction of an
+// encode; it exists for the wire container's integrity check.
+__global__ void __launch_bounds__(256) k_block_crc32(const uint8_t* payload, const uint64_t* offsets, int64_t nblocks,
+                                                     uint32_t* crc) {
+  __shared__ uint32_t tab[4][256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = (uint32_t)i;
+    for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+    tab[0][i] = c;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = tab[0][i];
+    for (int t = 1; t < 4; ++t) {
+      c = (c >> 8) ^ tab[0][c & 0xFFu];
+      tab[t][i] = c;
+    }
+  }
+  __syncthreads();
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  const uint64_t o0 = offsets[b], o1 = offsets[b + 1];
+  const uint8_t* p = payload + o0;
+  uint64_t n = o1 > o0 ? o1 - o0 : 0;
+  uint32_t c = 0xFFFFFFFFu;
+  while (n && (reinterpret_cast<uintptr_t>(p) & 3u)) {
+    c = (c >> 8) ^ tab[0][(c ^ *p++) & 0xFFu];
+    --n;
+  }
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
+  for (; n >= 4; n -= 4) {
+    const uint32_t x = c ^ __ldg(w++);
+    c = tab[3][x & 0xFFu] ^ tab[2][(x >> 8) & 0xFFu] ^ tab[1][(x >> 16) & 0xFFu] ^ tab[0][x >> 24];
+  }
+  p = reinterpret_cast<const uint8_t*>(w);
+  while (n--) c = (c >> 8) ^ tab[0][(c ^ *p++) & 0xFFu];
+  crc[b] = c ^ 0xFFFFFFFFu;
+}
+
+cudaError_t launch_block_crc32(const uint8_t* payload, const uint64_t* offsets, int64_t nblocks, uint32_t* crc,
+                               cudaStream_t s) {
+  ProfScope ps("block_crc32", s);
+  k_block_crc32<<<(unsigned)((nblocks + 255) / 256), 256, 0, s>>>(payload, offsets, nblocks, crc);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ device-length copy (P2P)
+// The length lives in device memory, so a pipelined transfer never syncs to
+// learn a data-dependent payload size.  16-byte vectors when both ends are
+// 16-byte aligned (blob buffers are), bytes otherwise.
+__global__ void __launch_bounds__(256) k_copy_device_length(uint8_t* dst, const uint8_t* src,
+                                                            const uint64_t* nbytes_dev, int64_t max_bytes) {
+  const uint64_t want = *nbytes_dev;
+  const uint64_t n = want < (uint64_t)max_bytes ? want : (uint64_t)max_bytes;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0) {
+    const uint64_t nv = n >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint64_t i = tid; i < nv; i += stride) d4[i] = s4[i];
+    for (uint64_t i = (nv << 4) + tid; i < n; i += stride) dst[i] = src[i];
+  } else {
+    for (uint64_t i = tid; i < n; i += stride) dst[i] = src[i];
+  }
+}
+
+cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes,
+                                      cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (max_bytes / 16 + 255) / 256 + 1;
+  const int64_t cap = (int64_t)sms * 4;
+  ProfScope ps("copy_device_length", s);
+  k_copy_device_length<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(
+      reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), nbytes_dev, max_bytes);
+  return cudaGetLastError();
+}
+
 }  // namespace kvc

@@ -667,8 +667,7 @@ bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows) {
 template <int MODE, int G, int W>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   auto k = k_enc128<MODE, G, W>;
-  static std::once_flag once;
-  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes); });
+  set_max_dyn_smem<k_enc128<MODE, G, W>>(kSmemBytes);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kSmemBytes);
   if (per_sm < 1) per_sm = 1;

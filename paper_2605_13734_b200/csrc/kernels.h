@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "kvc_internal.h"
 
 namespace kvc {
@@ -87,6 +89,20 @@ struct FusedArgs {
   float rl[9];
 };
 
+// cudaFuncSetAttribute is per device: raise a kernel's dynamic shared memory
+// limit once per (kernel, device) of the process
+template <auto K>
+inline void set_max_dyn_smem(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+}
+
 template <class A>
 __device__ __forceinline__ int64_t out_index(const A& a, int64_t lh, int64_t t, int64_t c) {
   if (!a.paged) return (lh * a.g.T + t) * a.g.C + c;
@@ -131,6 +147,10 @@ cudaError_t launch_codec_decode(const CodecArgs& a, int sm_count, cudaStream_t s
 // block offsets (exclusive scan of sizes) + gather of slots into the payload
 cudaError_t launch_codec_finish(const CodecArgs& a, cudaStream_t s);
 cudaError_t launch_check_payload(const CodecArgs& a, cudaStream_t s);
+cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes,
+                                      cudaStream_t s);
+cudaError_t launch_block_crc32(const uint8_t* payload, const uint64_t* offsets, int64_t nblocks, uint32_t* crc,
+                               cudaStream_t s);
 
 // fused quantize + range code (fused_rc.cu)
 bool fused_rc_applicable(const Geo& g);

@@ -315,8 +315,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <int W, bool AFF>
 cudaError_t launch_enc_u(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   auto k = k_enc_uchan128<W, AFF>;
-  static std::once_flag once;
-  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kUSmem); });
+  set_max_dyn_smem<k_enc_uchan128<W, AFF>>(kUSmem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kUThreads, kUSmem);
   if (per_sm < 1) per_sm = 1;
@@ -331,8 +330,7 @@ template <int W, bool AFF, typename Tout>
 cudaError_t launch_dec_u(const DecArgs& a, int sm_count, cudaStream_t s) {
   auto k = k_dec_uchan128<W, AFF, Tout>;
   const int smem = kUT * 128 * (int)sizeof(Tout) + 128 * 4 * 8 * 4 + 128 * 8 * 4 + 16;
-  static std::once_flag once;
-  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  set_max_dyn_smem<k_dec_uchan128<W, AFF, Tout>>(smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kUThreads, smem);
   if (per_sm < 1) per_sm = 1;

@@ -22,7 +22,7 @@ def lib():
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "kvc.h")).read()
-    return sorted(set(re.findall(r"\b(kvc_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(kvc_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_exports_every_declared_symbol(lib):
