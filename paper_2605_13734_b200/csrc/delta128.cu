@@ -129,8 +129,9 @@ __global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a) {
     if (tile + 1 < ntiles) commit(pf, buf ^ 1);
     __syncthreads();
   }
-  flags = __syncthreads_or(flags);
-  if (threadIdx.x == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 }  // namespace

@@ -498,8 +498,9 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     }
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
-  flags = __syncthreads_or(flags);
-  if (tid == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 // ------------------------------------------------------------ decode kernel
@@ -632,8 +633,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
       for (int k = 0; k < 16; ++k) o[k] = make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
     }
   }
-  flags = __syncthreads_or(flags);
-  if (threadIdx.x == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 // -------------------------------------------------------- host: tensor map

@@ -365,10 +365,12 @@ __global__ void __launch_bounds__(kFThreads) k_fused_tok_decode(const FusedArgs 
     for (int gq = 0; gq < 4; ++gq) {
       const float s = __half2float(__ushort_as_half(half_at(s4, gq)));
       const float z = __half2float(__ushort_as_half(half_at(z4, gq)));
+      // z + sym*s is non-finite for some symbol iff s or z is (|z|, s <= 65504,
+      // sym <= 15: no fp32 overflow; 0*inf is NaN), so one check per group
+      if (live && !(isfinite(s) && isfinite(z))) chk = 1.0f;
       decode32<W>(d, m, row * 128 + gq * 32, s, z, 0xffffffffu, [&](int k, const float* v) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          chk = live ? __fmaf_rn(v[i], 0.0f, chk) : chk;
           stage_value<Tout>(tile, lane, 8 * k + i, kStride, v[i]);
         }
       });
@@ -522,10 +524,10 @@ __global__ void __launch_bounds__(kFThreads) k_fused_chan_decode(const FusedArgs
     const float z = __half2float(__ushort_as_half(half_at(z4, gi & 3)));
     // this lane's destination row: token t0 + 32 gi + lane, channels c0 .. c0+31
     Tout* mine = reinterpret_cast<Tout*>(a.out) + out_index(a, cm.lh, t0 + gi * 32 + lane, c0);
+    if (!(isfinite(s) && isfinite(z))) chk = 1.0f;  // see k_fused_tok_decode
     decode32<W>(d, m, gi * 32, s, z, 0xffffffffu, [&](int k, const float* v) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        chk = __fmaf_rn(v[i], 0.0f, chk);
         stage_value<Tout>(tile, 8 * k + i, lane, kStride, v[i]);
       }
     });

@@ -278,8 +278,9 @@ __global__ void __launch_bounds__(256) k_encode_generic(EncArgs a, int TT) {
       pack_segment(a.packed, bit, sym + c * TT, 1, nt, g.bits, lane, 32);
     }
   }
-  flags = __syncthreads_or(flags);
-  if (threadIdx.x == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 // ------------------------------------------------------------ generic decode
@@ -352,8 +353,9 @@ __global__ void __launch_bounds__(256) k_decode_generic(DecArgs a, int TT) {
     if (!isfinite(v)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
     store_f32(out, out_index(a, lh, t0 + t, c), v);
   }
-  flags = __syncthreads_or(flags);
-  if (threadIdx.x == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 // delta decode: fp64 running sum along tokens per (head, channel) column,

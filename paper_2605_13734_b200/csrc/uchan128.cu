@@ -204,8 +204,9 @@ __global__ void __launch_bounds__(kUThreads, 3) k_enc_uchan128(const __grid_cons
     // __syncthreads, which every thread reaches after finishing these stores
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
-  flags = __syncthreads_or(flags);
-  if (tid == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 // ------------------------------------------------------------------ decode
@@ -295,8 +296,9 @@ __global__ void __launch_bounds__(kUThreads, 3) k_dec_uchan128(const DecArgs a) 
     }
     __syncthreads();
   }
-  flags = __syncthreads_or(flags);
-  if (tid == 0 && flags) atomicOr(a.status, flags);
+  // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -297,3 +297,28 @@ def test_fused_uchan_rejects_corruption():
     codec.decode(blob)
     with pytest.raises(_native.CodecError):
         codec.check(decoding=True)
+
+
+@pytest.mark.parametrize("sid", ["t=identity;q=uniform,b=2,g=32;c=entropy", "t=identity;q=uchan,b=2,g=32;c=entropy",
+                                 "t=identity;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=4,g=32;c=none"])
+def test_fp16_overflow_group_matches_reference_and_decode_raises(sid):
+    """A group whose range exceeds fp16 gets an infinite scale exactly as in
+    the reference (quantize.py:146); encode succeeds with identical bytes, and
+    decoding that blob yields non-finite values, which the reference's
+    KVTensor rejects (tensors.py:41-42) -> ValueError."""
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (1, 2, 1024, 128)
+    v, _ = oracle.generate_kv(*shape, seed=8)
+    v[0, 1, 100, 3] = 1.5e6  # after the Hadamard still ~1.3e5 > 65504
+    v[0, 1, 100, 40] = -1.2e6
+    tb, vb = bf16_exact(v)
+    ref = oracle.encode_blob(vb, None, sid, block=1024)
+    codec = KVCodec(sid, shape, out_dtype=torch.float32, block_symbols=1024)
+    blob = codec.encode(tb.cuda())
+    codec.check()
+    assert blob.metadata_bytes() == ref["metadata"]
+    assert blob.payload_bytes() == ref["payload"]
+    codec.decode(blob)
+    with pytest.raises(ValueError):
+        codec.check(decoding=True)
