@@ -504,21 +504,37 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
 }
 
 // ------------------------------------------------------------ decode kernel
-template <int G>
-__device__ __forceinline__ void dequant64(float* y, int cb0, int cb1, int64_t row, const __half* scales,
+// zero + symbol*scale (quantize.py:178) for the thread's 64 values.  With
+// FOLD (inverse Hadamard follows, decode held to tolerance) the 1/sqrt(128)
+// of the inverse is folded into scale and zero and the dequantization is one
+// FMA.  Returns false if a group's scale or zero is not finite -- the only
+// way a dequantized or Hadamard-mixed value can be non-finite (|z|, s <=
+// 65504, symbols <= 255: no fp32 overflow).
+template <int G, bool FOLD>
+__device__ __forceinline__ bool dequant64(float* y, int cb0, int cb1, int64_t row, const __half* scales,
                                           const __half* zeros) {
+  bool finite = true;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int cb = c ? cb1 : cb0;
 #pragma unroll
     for (int j = 0; j < (G < 32 ? 32 / G : 1); ++j) {
       const int64_t gi = row * (128 / G) + (cb + j * G) / G;
-      const float s = __half2float(scales[gi]), z = __half2float(zeros[gi]);
+      float s = __half2float(scales[gi]), z = __half2float(zeros[gi]);
+      finite &= isfinite(s) && isfinite(z);
       constexpr int n = G < 32 ? G : 32;
+      if (FOLD) {
+        s = __fmul_rn(s, 0.08838834764831845f);  // RN32(1/sqrt(128))
+        z = __fmul_rn(z, 0.08838834764831845f);
 #pragma unroll
-      for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fadd_rn(z, __fmul_rn(y[32 * c + j * n + i], s));
+        for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fmaf_rn(y[32 * c + j * n + i], s, z);
+      } else {
+#pragma unroll
+        for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fadd_rn(z, __fmul_rn(y[32 * c + j * n + i], s));
+      }
     }
   }
+  return finite;
 }
 
 template <int MODE, typename Tout, int G, int W>
@@ -563,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
       unpack32<W>(src + cb0 * W / 8, y);
       unpack32<W>(src + cb1 * W / 8, y + 32);
     }
-    dequant64<G>(y, cb0, cb1, row, scales, zeros);
+    const bool groups_finite = dequant64<G, MODE == M_HADAMARD>(y, cb0, cb1, row, scales, zeros);
     if (MODE == M_HADAMARD) {
       // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
       // (decode is held to tolerance): in-thread stages over channel bits
@@ -600,8 +616,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
           y[32 + k] = r - v;
         }
       }
-#pragma unroll
-      for (int i = 0; i < 64; ++i) y[i] = __fmul_rn(y[i], 0.08838834764831845f);  // RN32(1/sqrt(128))
     } else if (MODE == M_AFFINE) {
       const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
       const __half* scl = mu + g.LH * 128;
@@ -610,10 +624,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
         y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
     }
     if (!valid) continue;
-    float chk = 0.0f;
+    if (MODE == M_AFFINE) {  // y * (1/a) + mu can overflow for a tiny fp16 a
+      float chk = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
-    if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+      for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
+      if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+    } else if (!groups_finite) {
+      flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+    }
     Tout* out = reinterpret_cast<Tout*>(a.out) + out_index(a, lh, t, 64 * half);
     if constexpr (sizeof(Tout) == 2) {
       uint4* o = reinterpret_cast<uint4*>(out);

@@ -3,8 +3,8 @@
 //
 // Bit-exact with codecs.py:181-331 per block; one thread per block.  The
 // order-0 model (codecs.py:188-242) is ONE u16 Fenwick tree of frequencies
-// per thread in shared memory (512 B at A = 256), element j of thread t at
-// [j][t] so a warp's accesses to the same node are conflict-free; a symbol's
+// per thread in shared memory (512 B at A = 256), node pairs of thread t in
+// word [q][t] so a warp's accesses are bank-conflict-free; a symbol's
 // frequency is a Fenwick point query, so no separate frequency array is kept
 // and twice as many blocks fit per SM.  Prefix / point / update paths are
 // known from the symbol up front, so their shared loads issue together.
@@ -32,12 +32,17 @@ __host__ __device__ constexpr int halving_at() {
 template <int W>
 struct LModel {
   static constexpr int A = 1 << W;
-  uint16_t* tree;  // node j (1..A) at tree[(j - 1) * kLThreads]
+  // nodes j-1 = 2q, 2q+1 of a thread share one 32-bit word, word q of thread
+  // t at [q][t]: every lane of a warp hits its own bank whatever node it reads
+  uint16_t* tree;
   uint32_t total;
-  __device__ __forceinline__ uint32_t T(uint32_t j) const { return tree[(j - 1) * kLThreads]; }
-  __device__ __forceinline__ void set(uint32_t j, uint32_t v) { tree[(j - 1) * kLThreads] = (uint16_t)v; }
+  __device__ __forceinline__ static uint32_t at(uint32_t j) {
+    return (((j - 1) >> 1) * kLThreads) * 2 + ((j - 1) & 1);
+  }
+  __device__ __forceinline__ uint32_t T(uint32_t j) const { return tree[at(j)]; }
+  __device__ __forceinline__ void set(uint32_t j, uint32_t v) { tree[at(j)] = (uint16_t)v; }
   __device__ void init(uint16_t* base, int lane) {
-    tree = base + lane;
+    tree = base + 2 * lane;
     for (uint32_t j = 1; j <= (uint32_t)A; ++j) set(j, j & (0u - j));  // all frequencies 1
     total = A;
   }
@@ -102,17 +107,27 @@ struct LModel {
   // (codecs.py:214-225, :290-292) since a <= x // unit <=> a * unit <= x and
   // prefix(A-1) <= total - 1; plo = unit * prefix(s).  No overflow: partial
   // sums stay <= unit * total <= range.
-  __device__ __forceinline__ uint32_t find_scaled(uint32_t x, uint32_t unit, uint32_t& plo) const {
-    uint32_t pos = 0, acc = 0;
+  //
+  // The same descent also yields phi = unit * prefix(s+1) with no frequency
+  // query: node T(pos+bit) rejected at the last rejecting level covers
+  // [s+1 - lowbit(s+1), s+1) (every later level was accepted, so s+1's low
+  // bit is that level), hence unit * prefix(s+1) is exactly the rejected
+  // candidate acc + unit * T(pos+bit); with no rejection s = A-1 and
+  // prefix(A) = total.
+  __device__ __forceinline__ uint32_t find_scaled(uint32_t x, uint32_t unit, uint32_t& plo, uint32_t& phi) const {
+    uint32_t pos = 0, acc = 0, rej = unit * total;
 #pragma unroll
     for (uint32_t bit = A / 2; bit; bit >>= 1) {
       const uint32_t v = acc + unit * T(pos + bit);
       if (v <= x) {
         acc = v;
         pos += bit;
+      } else {
+        rej = v;
       }
     }
     plo = acc;
+    phi = rej;
     return pos;
   }
   // largest s with prefix(s) <= target (codecs.py:214-225); cum = prefix(s)
@@ -210,10 +225,9 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   for (int i = 0; i < n; ++i) {
     const uint32_t unit = (i < H) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
     // code < low only in a malformed stream; offset() reads 0 -> symbol 0
-    uint32_t plo;
-    const uint32_t s = m.find_scaled(d.offset(), unit, plo);
-    const uint32_t fr = m.freq(s);
-    d.advance(plo, plo + unit * fr);
+    uint32_t plo, phi;
+    const uint32_t s = m.find_scaled(d.offset(), unit, plo, phi);
+    d.advance(plo, phi);
     m.bump(s);
     acc = (acc << W) | s;
     nacc += W;
