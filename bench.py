@@ -423,16 +423,33 @@ def main():
     kernels = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] / prof_steps} for k, v in prof.items()}
 
     # ---------------- end-to-end through the public API with host buffers
+    # paper_2605_13734_b200.hostpath.HostRoundTrip: pinned host KV -> H2D ->
+    # encode -> wire into pinned host memory -> H2D -> decode, pipelined by
+    # layer chunks across copy engines / PCIe / SMs; the step's result is the
+    # reconstruction squared error, read back to the host.
     e2e = None
     if not args.no_e2e and not paged:
+        from paper_2605_13734_b200.hostpath import HostRoundTrip
+
         host_in = [t["kv"].cpu().pin_memory() for t in tensors]
         dev_in = [torch.empty_like(t["kv"]) for t in tensors]
-        host_pay = [torch.empty(int(t["blob"].payload_nbytes() * 1.05) + 4096, dtype=torch.uint8).pin_memory()
-                    for t in tensors]
-        host_meta = [torch.empty(t["codec"].metadata_bytes, dtype=torch.uint8).pin_memory() for t in tensors]
-        rx = [t["codec"].alloc_blob() for t in tensors]
+        L_rank = tensors[0]["kv"].shape[0]
+        chunk = max(1, min(8, L_rank // 4)) if L_rank >= 4 else L_rank
+        rts = [HostRoundTrip(t["sid"], tuple(t["kv"].shape), chunk_layers=chunk, block_symbols=BLOCK, device=dev,
+                             wire_bytes_hint=t["blob"].payload_nbytes()) for t in tensors]
+        outs = [t["out"] for t in tensors]
+        err = torch.zeros((), dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            err.zero_()
+            for rt, h, d_in, o in zip(rts, host_in, dev_in, outs):
+                rt.run(h, d_in, o, err)
+            return err.item()  # D2H of the step's result (syncs)
+
+        e2e_step()  # warm-up (plans, pinned buffers)
+        for rt in rts:
+            rt.check()
         e2e_steps = max(1, min(3, args.steps))
-        h2d = d2h = 0
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -440,43 +457,22 @@ def main():
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(e2e_steps):
-            h2d = d2h = 0
-            acc = torch.zeros((), dtype=torch.float64, device=dev)
-            for i, t in enumerate(tensors):
-                dev_in[i].copy_(host_in[i], non_blocking=True)
-                h2d += host_in[i].numel() * 2
-                b = t["codec"].encode(dev_in[i], out=t["blob"])
-                n = b.payload_nbytes()  # sync: size of the wire payload
-                host_pay[i][:n].copy_(b.payload[:n], non_blocking=True)
-                host_meta[i].copy_(b.metadata, non_blocking=True)
-                d2h += n + b.metadata.numel()
-                off_h = None
-                if b.offsets is not None:
-                    off_h = b.offsets[: b.nblocks + 1].cpu()
-                    d2h += 8 * (b.nblocks + 1)
-                # receiver side: host wire buffers -> HBM -> decode
-                r = rx[i]
-                r.payload[:n].copy_(host_pay[i][:n], non_blocking=True)
-                r.metadata.copy_(host_meta[i], non_blocking=True)
-                h2d += n + b.metadata.numel()
-                if off_h is not None:
-                    r.offsets[: b.nblocks + 1].copy_(off_h, non_blocking=True)
-                    h2d += 8 * (b.nblocks + 1)
-                r.nblocks, r._nbytes = b.nblocks, n
-                outp = t["codec"].decode(r, out=t["out"])
-                acc += ((outp.float() - dev_in[i].float()) ** 2).sum(dtype=torch.float64)
-            _ = acc.item()  # the step's result: reconstruction squared error
-            d2h += 8
+            e2e_step()
         s1.record()
         torch.cuda.synchronize()
         e2e_ms = s0.elapsed_time(s1) / e2e_steps
+        wire = sum(rt.wire_bytes() for rt in rts)
+        h2d = sum(h.numel() * 2 for h in host_in) + wire
+        d2h = wire + 8
         if world > 1:
             tt = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
         e2e = {"value": round(world * V_rank / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3),
-               "path": "pinned host KV -> H2D -> KVCodec.encode -> D2H wire blob -> H2D -> KVCodec.decode -> D2H error scalar"}
+               "chunk_layers": chunk,
+               "path": "pinned host KV -> H2D -> encode -> wire to pinned host -> H2D -> decode -> D2H squared-error "
+                       "scalar (hostpath.HostRoundTrip, layer-chunk pipeline)"}
 
     if rank == 0:
         line = {

@@ -42,6 +42,7 @@ EXPORTS = (
     "kvc_block_crc32",
     "kvc_copy_device_length",
     "kvc_enable_peer_access",
+    "kvc_sq_error",
 )
 
 
@@ -108,6 +109,8 @@ def lib() -> ctypes.CDLL:
     L.kvc_copy_device_length.restype = I32
     L.kvc_enable_peer_access.argtypes = [I32, I32]
     L.kvc_enable_peer_access.restype = I32
+    L.kvc_sq_error.argtypes = [P, P, I64, I32, P, P]
+    L.kvc_sq_error.restype = I32
     _lib = L
     return L
 

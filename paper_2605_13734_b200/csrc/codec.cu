@@ -434,4 +434,69 @@ cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------ squared error sum
+template <typename T>
+__global__ void __launch_bounds__(256) k_sq_error(const T* a, const T* b, int64_t n, double* out) {
+  constexpr int kVec = 16 / sizeof(T);
+  const int64_t nv = n / kVec;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  const uint4* a4 = reinterpret_cast<const uint4*>(a);
+  const uint4* b4 = reinterpret_cast<const uint4*>(b);
+  for (int64_t i = tid; i < nv; i += stride) {
+    const uint4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
+    float part = 0.0f;  // <= 8 terms in fp32, then fp64
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (sizeof(T) == 2) {
+        const float d0 = __uint_as_float(xw[k] << 16) - __uint_as_float(yw[k] << 16);
+        const float d1 = __uint_as_float(xw[k] & 0xFFFF0000u) - __uint_as_float(yw[k] & 0xFFFF0000u);
+        part = __fmaf_rn(d0, d0, __fmaf_rn(d1, d1, part));
+      } else {
+        const float d = __uint_as_float(xw[k]) - __uint_as_float(yw[k]);
+        part = __fmaf_rn(d, d, part);
+      }
+    }
+    acc += (double)part;
+  }
+  for (int64_t i = nv * kVec + tid; i < n; i += stride) {
+    float fa, fb;
+    if constexpr (sizeof(T) == 2) {
+      fa = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(a)[i] << 16);
+      fb = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(b)[i] << 16);
+    } else {
+      fa = reinterpret_cast<const float*>(a)[i];
+      fb = reinterpret_cast<const float*>(b)[i];
+    }
+    acc += (double)(fa - fb) * (double)(fa - fb);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    atomicAdd(out, t);
+  }
+}
+
+cudaError_t launch_sq_error(const void* a, const void* b, int64_t n, int dtype, double* out, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n / 8 + 255) / 256 + 1;
+  const int64_t cap = (int64_t)sms * 8;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  ProfScope ps("sq_error", s);
+  if (dtype == KVC_DTYPE_BF16)
+    k_sq_error<uint16_t><<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(a), reinterpret_cast<const uint16_t*>(b), n, out);
+  else
+    k_sq_error<float><<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(a), reinterpret_cast<const float*>(b), n, out);
+  return cudaGetLastError();
+}
+
 }  // namespace kvc
