@@ -263,6 +263,13 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   p.ws_slots = off; off = align_up(off + p.max_blocks * p.slot_bytes, 256);
   p.ws_sizes = off; off = align_up(off + 8 * (p.max_blocks + 1), 256);
   p.ws_scan = off; off = align_up(off + p.scan_bytes, 256);
+  // fused Hadamard encode: list of rows for the exact fixup pass (one int32
+  // per token row at most, plus the count)
+  p.ws_fix = -1;
+  if (g.transform == T_HADAMARD && fast128_applicable(g) && g.in_dtype == KVC_DTYPE_BF16) {
+    p.ws_fix = off;
+    off = align_up(off + 16 + 4 * g.LH * g.T, 256);
+  }
   // large-alphabet entropy encode precomputes its model per batch of blocks
   // (rc_large.cu): 4 bytes per symbol, batches of up to 2^18 blocks (enough
   // coder threads to fill the GPU; at most 2 GB at 2048-symbol blocks)
@@ -396,6 +403,12 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
     int64_t bytes = (g.E * ((g.quant == Q_UNIFORM || g.quant == Q_UCHAN) ? g.bits : g.hi) + 7) / 8 + 8;
     if ((e = cudaMemsetAsync(a.packed, 0, (size_t)bytes, s)) != cudaSuccess) return cuda_fail(e, "memset");
   }
+  const bool fix = p.ws_fix >= 0;
+  if (fix) {
+    a.fix_count = reinterpret_cast<uint32_t*>(ws + p.ws_fix);
+    a.fix_rows = reinterpret_cast<int32_t*>(ws + p.ws_fix + 16);
+    if ((e = cudaMemsetAsync(a.fix_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e, "memset");
+  }
   if (fast128_applicable(g))
     e = launch_encode_fast128(a, p.sm_count, s);
   else if (uchan128_applicable(g))
@@ -403,6 +416,9 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
   else
     e = launch_encode_generic(a, s);
   if (e != cudaSuccess) return cuda_fail(e, "encode kernel");
+  if (fix && fast128_applicable(g) && g.in_dtype == KVC_DTYPE_BF16 && g.LH * g.T < (1ll << 31)) {
+    if ((e = launch_encode_fixup(a, s)) != cudaSuccess) return cuda_fail(e, "encode fixup");
+  }
   if (g.codec != C_NONE) {
     CodecArgs c;
     memset(&c, 0, sizeof c);

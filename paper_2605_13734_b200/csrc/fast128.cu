@@ -368,10 +368,33 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     float y[64];
     int cb0, cb1;
     bool hadlayout = false;
+    bool need_fix = false;  // Hadamard: this row is re-encoded exactly by k_encode_fixup
+    const uint32_t flags_before = flags;
     if (MODE == M_HADAMARD) {
-      // the 2^-896 reinterpretation maps NaN / inf to finite doubles: check the
-      // bf16 input explicitly (tensors.py:41-42)
-      if (nonfinite64_bf16(wv)) nanacc = 1.0f;
+      // Input range of the whole row (this half and the partner's): with every
+      // |x| in [2^-100, 2^101) no Hadamard output can overflow f32 or be a
+      // nonzero f32 subnormal, so the rounding below needs only the
+      // near-midpoint test.  NaN / inf inputs (which the 2^-896
+      // reinterpretation would turn into finite doubles) show up here too
+      // (tensors.py:41-42).  Zeros, extreme magnitudes and near-midpoint
+      // results send the row to the exact fixup pass (k_encode_fixup).
+      bool row_ok;
+      {
+        uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
+#pragma unroll
+        for (int k = 1; k < 32; ++k) {
+          const uint32_t aw = wv[k] & 0x7FFF7FFFu;
+          amx = bmax2(amx, aw);
+          amn = bmin2(amn, aw);
+        }
+        amx = bmax2(amx, __byte_perm(amx, 0, 0x1032));
+        amn = bmin2(amn, __byte_perm(amn, 0, 0x1032));
+        if ((amx & 0x7F80u) == 0x7F80u) nanacc = 1.0f;
+        amx = bmax2(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
+        amn = bmin2(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
+        const uint32_t emax = (amx >> 7) & 0xFFu, emin = (amn >> 7) & 0xFFu;
+        row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+      }
       double f[64];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -408,25 +431,18 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
           f[32 + k] = r - v;
         }
       }
-      // branch-free rounding per 8 values; the rare exact fallback is a cold call
+      // RN32(RN64(S / sqrt n)) as one F2F of RN64(S * RN64(1/sqrt n)); the two
+      // differ only within 4 ulp64 of an f32 rounding midpoint (numerics.cuh)
+      bool mid = false;
 #pragma unroll
-      for (int c8 = 0; c8 < 64; c8 += 8) {
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          bool sl;
-          y[c8 + j] = hadamard_fast(f[c8 + j], a.hk, sl);
-          any |= sl;
-        }
-        if (any) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            bool sl;
-            hadamard_fast(f[c8 + j], a.hk, sl);
-            if (sl) y[c8 + j] = hadamard_slow(f[c8 + j], a.hc, &flags);
-          }
-        }
+      for (int i = 0; i < 64; ++i) {
+        const double q = f[i] * a.hk;
+        mid |= ((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x0FFFFFFCu <= 8u;
+        y[i] = __double2float_rn(q);
       }
+      need_fix = !row_ok || mid;
+      need_fix |= __shfl_xor_sync(0xffffffffu, (int)need_fix, 1) != 0;
+      if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       cb0 = 32 * half;
       cb1 = 64 + 32 * half;
       hadlayout = true;
@@ -496,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
         pack32_store<W>(y + 32, out + cb1 * W / 8);
       }
     }
+    if (need_fix) flags = flags_before;  // the fixup pass sets this row's flags exactly
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)

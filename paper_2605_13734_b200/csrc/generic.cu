@@ -155,15 +155,11 @@ __device__ void pack_segment(uint8_t* out, int64_t bit, const uint8_t* s, int64_
 }
 
 // ------------------------------------------------------------ generic encode
+// one tile of TT token rows (lh, t0 .. t0+nt-1), all of it in shared memory
 template <typename Tin>
-__global__ void __launch_bounds__(256) k_encode_generic(EncArgs a, int TT) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ void encode_tile(const EncArgs& a, int TT, int64_t lh, int64_t t0, int nt, unsigned char* smem) {
   const Geo& g = a.g;
   const int64_t C = g.C, T = g.T;
-  const int64_t tiles = (T + TT - 1) / TT;
-  const int64_t lh = blockIdx.x / tiles;
-  const int64_t t0 = (blockIdx.x % tiles) * TT;
-  const int nt = (int)min((int64_t)TT, T - t0);
   float* y = reinterpret_cast<float*>(smem);  // [TT][C]
   float* prev = y + (int64_t)TT * C;          // [C]
   uint8_t* sym = reinterpret_cast<uint8_t*>(prev + C);  // quant-ordered symbols
@@ -281,6 +277,30 @@ __global__ void __launch_bounds__(256) k_encode_generic(EncArgs a, int TT) {
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(256) k_encode_generic(EncArgs a, int TT) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t tiles = (a.g.T + TT - 1) / TT;
+  const int64_t lh = blockIdx.x / tiles;
+  const int64_t t0 = (blockIdx.x % tiles) * TT;
+  encode_tile<Tin>(a, TT, lh, t0, (int)min((int64_t)TT, a.g.T - t0), smem);
+}
+
+// Exact re-encode of the token rows the fused Hadamard encode listed (rows
+// whose fast rounding it could not prove exact, fast128.cu): each CTA takes
+// list entries in turn and overwrites the row's bytes, scales and zeros.  The
+// count is read on the device, so the launch never waits on the host.
+__global__ void __launch_bounds__(256) k_encode_fixup(EncArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t n = *a.fix_count;
+  for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
+    const int64_t row = a.fix_rows[e];
+    const int64_t lh = row / a.g.T;
+    encode_tile<__nv_bfloat16>(a, 1, lh, row - lh * a.g.T, 1, smem);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------ generic decode
@@ -431,6 +451,17 @@ cudaError_t launch_encode_generic(const EncArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_encode_generic<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_encode_generic<float><<<(unsigned)tiles, 256, sm, s>>>(a, TT);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_fixup(const EncArgs& a, cudaStream_t s) {
+  const size_t sm = generic_encode_smem(a.g, 1);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ProfScope ps("encode_fixup", s);
+  cudaFuncSetAttribute(k_encode_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_encode_fixup<<<(unsigned)(2 * sms), 256, sm, s>>>(a);
   return cudaGetLastError();
 }
 

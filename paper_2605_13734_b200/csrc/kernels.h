@@ -20,6 +20,8 @@ struct EncArgs {
   uint32_t* status;
   double hk, hc;    // hadamard: 2^896 * RN64(1/sqrt(C)), RN64(sqrt(C))
   float rl[9];      // RN32(1 / (2^w - 1))
+  int32_t* fix_rows;    // fused Hadamard encode: rows left to the exact fixup pass
+  uint32_t* fix_count;
 };
 
 struct DecArgs {
@@ -115,6 +117,7 @@ cudaError_t launch_setup(const Geo& g, const uint8_t* meta, StreamTab* st, HeadE
 cudaError_t launch_write_classmap(const ClassBits& cb, uint8_t* dst, int nbytes, cudaStream_t s);
 cudaError_t launch_affine_calibrate(const Geo& g, const void* kv, uint8_t* meta, cudaStream_t s);
 cudaError_t launch_encode_generic(const EncArgs& a, cudaStream_t s);
+cudaError_t launch_encode_fixup(const EncArgs& a, cudaStream_t s);
 cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s);
 
 // fast head_dim-128 per-token kernels (fast128.cu); return false if not applicable

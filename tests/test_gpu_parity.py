@@ -322,3 +322,28 @@ def test_fp16_overflow_group_matches_reference_and_decode_raises(sid):
     codec.decode(blob)
     with pytest.raises(ValueError):
         codec.check(decoding=True)
+
+
+def test_hadamard_fast_path_adversarial_rows_are_exact():
+    """The fused Hadamard encode leaves rows with zeros, tiny / huge
+    magnitudes or near-midpoint results to the exact fixup pass
+    (k_encode_fixup); every row must still match the reference bit for bit."""
+    shape = (1, 2, 64, 128)
+    rng = np.random.default_rng(31)
+    v = rng.normal(size=shape).astype(np.float32)
+    v[0, 0, 1] = 0.0                                  # all-zero row
+    v[0, 0, 2, ::3] = 0.0                             # sparse zeros
+    v[0, 0, 3] *= 1e-33                               # tiny magnitudes (f32 subnormal outputs)
+    v[0, 0, 4, :64] *= 2.0 ** -40                     # exponent span 2^+-40 within a row
+    v[0, 0, 4, 64:] *= 2.0 ** 12
+    v[0, 1, 5] = 1.0                                  # constant row (most outputs exactly 0)
+    v[0, 1, 6, 7] = -3.0e-39                          # one tiny value in a normal row
+    for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=2,g=64;c=entropy"):
+        tb, vb = bf16_exact(v)
+        ref = oracle.encode_blob(vb, None, sid, block=256)
+        from paper_2605_13734_b200 import KVCodec
+        codec = KVCodec(sid, shape, out_dtype=torch.float32, block_symbols=256)
+        blob = codec.encode(tb.cuda())
+        codec.check()
+        assert blob.metadata_bytes() == ref["metadata"], sid
+        assert blob.payload_bytes() == ref["payload"], sid
