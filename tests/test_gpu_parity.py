@@ -347,3 +347,37 @@ def test_hadamard_fast_path_adversarial_rows_are_exact():
         codec.check()
         assert blob.metadata_bytes() == ref["metadata"], sid
         assert blob.payload_bytes() == ref["payload"], sid
+
+
+def test_whole_stream_entropy_and_rle_match_reference_blobs():
+    """with one codec block per width stream
+    (block_symbols >= the stream length) the payload IS the reference's
+    whole-tensor format (codecs.py:361-367: per width BE32 length +
+    range_encode(stream); rle over the packed stream), byte for byte, and the
+    per-thread coders handle the model halvings of long streams."""
+    from golden_io import items, load
+    from paper_2605_13734_b200 import KVCodec
+
+    g = load("pipeline_180.npz")
+    vals, imp = g["values"], g["importance"]
+    pays = items(g["payload"], g["payload_off"])
+    metas = items(g["metadata"], g["metadata_off"])
+    E = int(np.prod(vals.shape))
+    block = (E + 7) // 8 * 8
+    checked = 0
+    for k, sid in enumerate(g["ids"]):
+        sid = str(sid)
+        s = oracle.parse_id(sid)
+        if s.codec == "none" or (s.codec == "rle" and s.quant != "uniform"):
+            continue  # rle of two concatenated streams is not per-stream framing
+        cls = oracle.classify_heads(imp, s.rho) if s.quant == "mixed" else None
+        codec = KVCodec(sid, vals.shape, in_dtype=torch.float32, out_dtype=torch.float32, block_symbols=block)
+        blob = codec.encode(torch.from_numpy(vals).cuda(), head_classes=cls)
+        codec.check()
+        assert blob.payload_bytes() == pays[k], sid
+        assert blob.metadata_bytes() == metas[k], sid
+        out = codec.decode(blob).cpu().numpy()
+        codec.check(decoding=True)
+        assert np.array_equal(out.view(np.uint32), g["recon"][k].view(np.uint32)), sid
+        checked += 1
+    assert checked >= 60
