@@ -434,8 +434,11 @@ __global__ void __launch_bounds__(128) k_rc_large_code(CodecArgs a, int64_t b0, 
 template <int W>
 cudaError_t enc2_w(const CodecArgs& a, cudaStream_t s) {
   const int64_t total = a.max_blocks + 1;  // block ids 0 .. max_blocks
-  for (int64_t b0 = 0; b0 < total; b0 += a.model_blocks) {
-    const int64_t nb = min(a.model_blocks, total - b0);
+  // equal batches (a small last batch would leave the coder pass at low occupancy)
+  const int64_t nbatch = (total + a.model_blocks - 1) / a.model_blocks;
+  const int64_t per = (total + nbatch - 1) / nbatch;
+  for (int64_t b0 = 0; b0 < total; b0 += per) {
+    const int64_t nb = min(per, total - b0);
     k_rc_large_model<W><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(a, b0, nb);
     k_rc_large_code<W><<<(unsigned)((nb + 127) / 128), 128, 0, s>>>(a, b0, nb);
   }
