@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
 }
 
 // ------------------------------------------------------------ decode kernel
-// zero + symbol*scale (quantize.py:178) for the thread's 64 values.  With
-// FOLD (inverse Hadamard follows, decode held to tolerance) the 1/sqrt(128)
-// of the inverse is folded into scale and zero and the dequantization is one
-// FMA.  Returns false if a group's scale or zero is not finite -- the only
+// zero + symbol*scale (quantize.py:178) for the thread's 64 values, unfused
+// like the reference.  (FOLD = 1/sqrt(128) folded into scale and zero, one
+// FMA per value: measured 3% faster but it breaks the 1-bf16-ulp bound on
+// near-zero outputs, so the decode does not use it.)  Returns false if a group's scale or zero is not finite -- the only
 // way a dequantized or Hadamard-mixed value can be non-finite (|z|, s <=
 // 65504, symbols <= 255: no fp32 overflow).
 template <int G, bool FOLD>
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
       unpack32<W>(src + cb0 * W / 8, y);
       unpack32<W>(src + cb1 * W / 8, y + 32);
     }
-    const bool groups_finite = dequant64<G, MODE == M_HADAMARD>(y, cb0, cb1, row, scales, zeros);
+    const bool groups_finite = dequant64<G, false>(y, cb0, cb1, row, scales, zeros);
     if (MODE == M_HADAMARD) {
       // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
       // (decode is held to tolerance): in-thread stages over channel bits
@@ -633,6 +633,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
           y[32 + k] = r - v;
         }
       }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) y[i] = __fmul_rn(y[i], 0.08838834764831845f);  // RN32(1/sqrt(128))
     } else if (MODE == M_AFFINE) {
       const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
       const __half* scl = mu + g.LH * 128;
