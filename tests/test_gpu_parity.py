@@ -381,3 +381,25 @@ def test_whole_stream_entropy_and_rle_match_reference_blobs():
         assert np.array_equal(out.view(np.uint32), g["recon"][k].view(np.uint32)), sid
         checked += 1
     assert checked >= 60
+
+
+@pytest.mark.parametrize("sid", ["t=hadamard;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=2,g=64;c=entropy",
+                                 "t=hadamard;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=none"])
+def test_hadamard_decode_bf16_within_one_ulp(sid):
+    """decoded bf16 within 1 bf16 ulp of bf16(reference) on
+    paths with an inverse transform (the fused decode runs it in fp32)."""
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (2, 4, 256, 128)
+    v, imp = oracle.generate_kv(*shape, seed=17)
+    tb, vb = bf16_exact(v)
+    s = oracle.parse_id(sid)
+    cls = oracle.classify_heads(imp, s.rho) if s.quant == "mixed" else None
+    codec = KVCodec(sid, shape, block_symbols=1024)
+    out = codec.decode(codec.encode(tb.cuda(), head_classes=cls)).float().cpu().numpy()
+    codec.check(decoding=True)
+    ref = oracle.encode_blob(vb, imp, sid, block=1024)
+    rec = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, shape, block=1024)
+    ref_bf16 = torch.from_numpy(rec).to(torch.bfloat16).float().numpy()
+    ulp = np.abs(out - ref_bf16) / np.maximum(np.abs(ref_bf16) * 2.0 ** -7, 1e-30)
+    assert float(ulp.max()) <= 1.0 + 1e-6, (sid, float(ulp.max()))
