@@ -26,7 +26,7 @@ namespace {
 
 constexpr int kThreads = 128;            // 64 rows per tile
 constexpr int kRows = kThreads / 2;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kTileBytes = kThreads * 128;  // one 128 B half-row per thread
 constexpr int kSmemBytes = kStages * kTileBytes + 1024 + 64;
 
