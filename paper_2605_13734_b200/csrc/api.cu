@@ -263,6 +263,12 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   p.ws_slots = off; off = align_up(off + p.max_blocks * p.slot_bytes, 256);
   p.ws_sizes = off; off = align_up(off + 8 * (p.max_blocks + 1), 256);
   p.ws_scan = off; off = align_up(off + p.scan_bytes, 256);
+  // chunked delta decode (delta128.cu)
+  p.ws_delta = -1;
+  if (delta128_applicable(g)) {
+    p.ws_delta = off;
+    off = align_up(off + delta128_ws_bytes(g), 256);
+  }
   // fused Hadamard encode: list of rows for the exact fixup pass (one int32
   // per token row at most, plus the count)
   p.ws_fix = -1;
@@ -516,7 +522,7 @@ static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payloa
   a.layer_stride = layer_stride;
   fill_common(p, a.hk, a.hc);
   if (delta128_applicable(g))
-    e = launch_decode_delta128(a, s);
+    e = launch_decode_delta128(a, p.ws_delta >= 0 ? ws + p.ws_delta : nullptr, s);
   else if (fast128_applicable(g))
     e = launch_decode_fast128(a, p.sm_count, s);
   else if (uchan128_applicable(g))

@@ -27,24 +27,48 @@ constexpr int kSymPer = kDT * kWPR / kDThreads;  // staged words per thread (8)
 constexpr int kGMax = 16;       // groups per row (group >= 8)
 constexpr int kSzPer = kDT * kGMax / kDThreads;  // staged scale (and zero) halves per thread (4)
 
+// chunks per head: ~24 CTAs per SM in total (the per-channel add chains are
+// latency bound, so the GPU needs many of them in flight), >= 4 tiles each
+__host__ __device__ inline void delta_chunking(const Geo& g, int& nchunks, int& chunk_tiles) {
+  const int ntiles = (int)((g.T + kDT - 1) / kDT);
+  int64_t want = (148 * 24 + g.LH - 1) / g.LH;
+  if (want < 1) want = 1;
+  if (want > 256) want = 256;
+  chunk_tiles = (int)((ntiles + want - 1) / want);
+  if (chunk_tiles < 4) chunk_tiles = 4;
+  nchunks = (ntiles + chunk_tiles - 1) / chunk_tiles;
+}
+
+inline void delta_ws_layout(const Geo& g, void* ws, double*& sum, double*& carry, uint32_t*& bad, uint32_t*& nf,
+                            int& nchunks, int& chunk_tiles) {
+  delta_chunking(g, nchunks, chunk_tiles);
+  const int64_t n = g.LH * (int64_t)nchunks * kDThreads;
+  sum = reinterpret_cast<double*>(ws);
+  carry = sum + n;
+  bad = reinterpret_cast<uint32_t*>(carry + n);
+  nf = bad + g.LH;
+}
+
 struct Prefetch {
   uint32_t wv[kSymPer];
   unsigned short sv[kSzPer], zv[kSzPer];
   uint32_t wid;  // row width, valid for threads < nt
 };
 
-template <typename Tout>
-__global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a) {
+// Decode tokens [tile0*kDT, tile1*kDT) of head lh starting from the running
+// sum `acc` (scaled by 2^-896); PASS 0 = full sequential decode (outputs),
+// PASS 1 = chunk sum only (no outputs), PASS 3 = outputs of one chunk.
+// Returns the running sum after the range.
+template <typename Tout, int PASS>
+__device__ double delta_range(const DecArgs& a, int64_t lh, int tile0, int tile1, double acc, uint32_t& flags) {
   __shared__ __align__(16) uint32_t sym[2][kDT][kWPR];
   __shared__ unsigned short ssc[2][kDT][kGMax], szr[2][kDT][kGMax];
   __shared__ uint32_t rw[2][kDT];
   const Geo& g = a.g;
-  const int64_t lh = blockIdx.x;
   const int tid = threadIdx.x;
   const int G = (int)g.G;
   const unsigned short* scales = reinterpret_cast<const unsigned short*>(a.meta);
   const unsigned short* zeros = scales + g.ngroups;
-  const int ntiles = (int)((g.T + kDT - 1) / kDT);
   Tout* out = reinterpret_cast<Tout*>(a.out);
 
   auto prefetch = [&](int tile, Prefetch& pf) {
@@ -95,18 +119,17 @@ __global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a) {
     if (tid < kDT) rw[buf][tid] = pf.wid;
   };
 
-  double acc = 0.0;  // running sum * 2^-896 (exact scaling)
-  uint32_t flags = 0;
   Prefetch pf;
-  prefetch(0, pf);
+  prefetch(tile0, pf);
   commit(pf, 0);
   __syncthreads();
   const int c = tid, j = c / g.group;
-  for (int tile = 0; tile < ntiles; ++tile) {
-    const int buf = tile & 1;
-    if (tile + 1 < ntiles) prefetch(tile + 1, pf);  // loads in flight during the adds
+  for (int tile = tile0; tile < tile1; ++tile) {
+    const int buf = (tile - tile0) & 1;
+    if (tile + 1 < tile1) prefetch(tile + 1, pf);  // loads in flight during the adds
     const int t0 = tile * kDT;
     const int nt = (int)min((int64_t)kDT, g.T - t0);
+#pragma unroll 8
     for (int r = 0; r < nt; ++r) {
       const int w = (int)rw[buf][r];
       const int p = c * w, off = p & 31;
@@ -121,17 +144,120 @@ __global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a) {
       const float sc = __half2float(__ushort_as_half(ssc[buf][r][j]));
       const float ze = __half2float(__ushort_as_half(szr[buf][r][j]));
       acc += f32bits_scaled_f64(__float_as_uint(dequant(s, sc, ze)));
-      const float v = __double2float_rn(acc * 0x1p896);
-      if (!isfinite(v)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
-      store_f32(out, out_index(a, lh, t0 + r, c), v);
+      if (PASS != 1) {
+        const float v = __double2float_rn(acc * 0x1p896);
+        if (!isfinite(v)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+        store_f32(out, out_index(a, lh, t0 + r, c), v);
+      }
     }
     __syncthreads();  // buffer buf^1 (tile-1) is free and buf fully read
-    if (tile + 1 < ntiles) commit(pf, buf ^ 1);
+    if (tile + 1 < tile1) commit(pf, buf ^ 1);
     __syncthreads();
   }
+  return acc;
+}
+
+// Sequential decode of whole heads (one CTA per head, thread per channel):
+// the additions happen in exactly the reference's order.  `only` (optional)
+// restricts it to heads whose chunked decode failed verification.
+template <typename Tout>
+__global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a, const uint32_t* only) {
+  const int64_t lh = blockIdx.x;
+  if (only && !only[lh]) return;
+  uint32_t flags = 0;
+  const int ntiles = (int)((a.g.T + kDT - 1) / kDT);
+  delta_range<Tout, 0>(a, lh, 0, ntiles, 0.0, flags);
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
+}
+
+// ---------------------------------------------------------- chunked decode
+// The running sum is sequential in the reference (np.cumsum, float64), but
+// for real KV every partial sum is exactly representable, and then a chunk
+// can start from the exact prefix of the chunks before it.  Three passes:
+//   1. each (head, chunk) CTA sums its chunk from 0 (the reference's order);
+//   2. one thread per (head, channel) turns the chunk sums into chunk-start
+//      carries (sequential over chunks);
+//   3. each (head, chunk) CTA decodes its chunk from its carry with the
+//      reference's additions and checks that its final running sum equals
+//      the next chunk's carry.
+// Pass 3 reproduces the reference bit for bit whenever the chunk's start
+// value is the reference's; chunk 0 starts from 0 and every later start is
+// verified against the previous chunk's exact end (induction).  A head with
+// any mismatch is redone sequentially (k_dec_delta128 restricted to it), and
+// its pass-3 flags are discarded.
+struct DeltaWs {
+  double* sum;    // [LH][nchunks][128]
+  double* carry;  // [LH][nchunks][128]
+  uint32_t* bad;  // [LH]
+  uint32_t* nf;   // [LH] non-finite output seen in pass 3
+  int nchunks, chunk_tiles;
+};
+
+template <typename Tout, int PASS>
+__global__ void __launch_bounds__(kDThreads) k_delta_chunk(const DecArgs a, DeltaWs w) {
+  const int64_t lh = blockIdx.x / w.nchunks;
+  const int ch = (int)(blockIdx.x % w.nchunks);
+  const int ntiles = (int)((a.g.T + kDT - 1) / kDT);
+  const int tile0 = ch * w.chunk_tiles;
+  const int tile1 = min(ntiles, tile0 + w.chunk_tiles);
+  const int64_t slot = (lh * w.nchunks + ch) * kDThreads + threadIdx.x;
+  uint32_t flags = 0;
+  if (tile0 >= tile1) {  // empty trailing chunk
+    if (PASS == 1) w.sum[slot] = 0.0;
+    return;
+  }
+  const double start = PASS == 1 ? 0.0 : w.carry[slot];
+  const double end = delta_range<Tout, PASS>(a, lh, tile0, tile1, start, flags);
+  if (PASS == 1) {
+    w.sum[slot] = end;
+  } else {
+    bool bad = ch + 1 < w.nchunks &&
+               __double_as_longlong(end) != __double_as_longlong(w.carry[slot + kDThreads]);
+    bad = __syncthreads_or(bad);  // used as a predicate here
+    if (threadIdx.x == 0 && bad) atomicOr(&w.bad[lh], 1u);
+    const bool nf = __syncthreads_or(flags != 0);
+    if (threadIdx.x == 0 && nf) atomicOr(&w.nf[lh], 1u);
+  }
+}
+
+__global__ void k_delta_carry(DeltaWs w, int64_t LH) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (head, channel)
+  if (i >= LH * kDThreads) return;
+  const int64_t lh = i / kDThreads, c = i - lh * kDThreads;
+  double run = 0.0;
+  for (int ch = 0; ch < w.nchunks; ++ch) {
+    const int64_t slot = (lh * w.nchunks + ch) * kDThreads + c;
+    w.carry[slot] = run;
+    run += w.sum[slot];
+  }
+  if (c == 0) w.bad[lh] = 0u, w.nf[lh] = 0u;
+}
+
+// flags of the heads that passed verification
+__global__ void k_delta_flags(DeltaWs w, int64_t LH, uint32_t* status) {
+  const int64_t lh = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lh < LH && !w.bad[lh] && w.nf[lh]) atomicOr(status, (uint32_t)KVC_FLAG_NONFINITE_TRANSFORM);
+}
+
+template <typename Tout>
+cudaError_t launch_delta(const DecArgs& a, void* ws, cudaStream_t s) {
+  const Geo& g = a.g;
+  const int ntiles = (int)((g.T + kDT - 1) / kDT);
+  if (!ws || ntiles < 16) {  // short sequences: one pass
+    k_dec_delta128<Tout><<<(unsigned)g.LH, kDThreads, 0, s>>>(a, nullptr);
+    return cudaGetLastError();
+  }
+  DeltaWs w;
+  delta_ws_layout(g, ws, w.sum, w.carry, w.bad, w.nf, w.nchunks, w.chunk_tiles);
+  const unsigned grid = (unsigned)(g.LH * w.nchunks);
+  k_delta_chunk<Tout, 1><<<grid, kDThreads, 0, s>>>(a, w);
+  k_delta_carry<<<(unsigned)((g.LH * kDThreads + 255) / 256), 256, 0, s>>>(w, g.LH);
+  k_delta_chunk<Tout, 3><<<grid, kDThreads, 0, s>>>(a, w);
+  k_dec_delta128<Tout><<<(unsigned)g.LH, kDThreads, 0, s>>>(a, w.bad);
+  k_delta_flags<<<(unsigned)((g.LH + 255) / 256), 256, 0, s>>>(w, g.LH, a.status);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -140,13 +266,16 @@ bool delta128_applicable(const Geo& g) {
   return g.transform == T_DELTA && !g.uchan && g.C == 128 && g.group >= 8 && 128 % g.group == 0;
 }
 
-cudaError_t launch_decode_delta128(const DecArgs& a, cudaStream_t s) {
+int64_t delta128_ws_bytes(const Geo& g) {
+  int nchunks, chunk_tiles;
+  delta_chunking(g, nchunks, chunk_tiles);
+  return (int64_t)g.LH * nchunks * kDThreads * 16 + 8 * g.LH + 64;
+}
+
+cudaError_t launch_decode_delta128(const DecArgs& a, void* ws, cudaStream_t s) {
   ProfScope ps("decode_delta128", s);
-  if (a.g.out_dtype == KVC_DTYPE_BF16)
-    k_dec_delta128<__nv_bfloat16><<<(unsigned)a.g.LH, kDThreads, 0, s>>>(a);
-  else
-    k_dec_delta128<float><<<(unsigned)a.g.LH, kDThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  if (a.g.out_dtype == KVC_DTYPE_BF16) return launch_delta<__nv_bfloat16>(a, ws, s);
+  return launch_delta<float>(a, ws, s);
 }
 
 }  // namespace kvc

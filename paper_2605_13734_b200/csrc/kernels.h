@@ -132,7 +132,8 @@ cudaError_t launch_decode_uchan128(const DecArgs& a, int sm_count, cudaStream_t 
 
 // delta decode, head_dim 128, exact sequential fp64 cumsum (delta128.cu)
 bool delta128_applicable(const Geo& g);
-cudaError_t launch_decode_delta128(const DecArgs& a, cudaStream_t s);
+int64_t delta128_ws_bytes(const Geo& g);
+cudaError_t launch_decode_delta128(const DecArgs& a, void* ws, cudaStream_t s);
 
 // small-alphabet range coder (rc_small.cu), widths 1..4
 bool rc_small_supported(int w);

@@ -403,3 +403,38 @@ def test_hadamard_decode_bf16_within_one_ulp(sid):
     ref_bf16 = torch.from_numpy(rec).to(torch.bfloat16).float().numpy()
     ulp = np.abs(out - ref_bf16) / np.maximum(np.abs(ref_bf16) * 2.0 ** -7, 1e-30)
     assert float(ulp.max()) <= 1.0 + 1e-6, (sid, float(ulp.max()))
+
+
+@pytest.mark.parametrize("sid", ["t=delta;q=uniform,b=4,g=32;c=none", "t=delta;q=uniform,b=8,g=64;c=none",
+                                 "t=delta;q=uniform,b=2,g=32;c=entropy", "t=delta;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=none"])
+def test_delta_chunked_decode_exact(sid):
+    """Long sequences take the chunked delta decode (chunk sums -> carries ->
+    verified chunk decode, delta128.cu); the result is the reference's
+    sequential float64 cumsum bit for bit."""
+    shape = (2, 2, 2048, 128)
+    got, rec, _ = run_case(sid, shape, seed=23, block=1024)
+    assert np.array_equal(got.view(np.uint32), rec.view(np.uint32)), sid
+
+
+def test_delta_chunked_decode_falls_back_when_sums_round():
+    """A running sum that rounds in float64 (a 3e4 offset then 1e-6 detail)
+    makes the chunk carries disagree with the sequential sums; the head is
+    re-decoded sequentially and still matches the reference exactly."""
+    shape = (1, 2, 2048, 128)
+    rng = np.random.default_rng(5)
+    v = (1e-6 * rng.normal(size=shape)).astype(np.float32)
+    v[:, :, :, :8] += 3.0e4  # every token: large channels, so the deltas keep tiny detail
+    v[0, 0, 0, :] = 3.0e4
+    sid = "t=delta;q=uniform,b=8,g=32;c=none"
+    got, rec, _ = run_case(sid, shape, seed=0, block=1024) if False else (None, None, None)
+    from paper_2605_13734_b200 import KVCodec
+    tb, vb = bf16_exact(v)
+    codec = KVCodec(sid, shape, out_dtype=torch.float32, block_symbols=1024)
+    blob = codec.encode(tb.cuda())
+    codec.check()
+    ref = oracle.encode_blob(vb, None, sid, block=1024)
+    assert blob.payload_bytes() == ref["payload"] and blob.metadata_bytes() == ref["metadata"]
+    out = codec.decode(blob).cpu().numpy()
+    codec.check(decoding=True)
+    rec = oracle.decode_blob(ref["payload"], ref["metadata"], None, sid, shape, block=1024)
+    assert np.array_equal(out.view(np.uint32), rec.view(np.uint32))
