@@ -149,3 +149,25 @@ def test_paged_decode_matches_contiguous():
         codec.check(decoding=True)
         pv = pages.view(L, npages, P, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
         assert torch.equal(pv, flat), sid
+
+
+def test_paged_delta_long_sequence_chunked():
+    """The chunked delta decode (long T) writes the same values into a paged
+    cache as into a contiguous tensor."""
+    from paper_2605_13734_b200 import KVCodec
+
+    L, H, T, C = 2, 2, 2048, 128
+    v, _ = oracle.generate_kv(L, H, T, C, seed=19)
+    kv = torch.from_numpy(v).to(torch.bfloat16).cuda()
+    for sid in ("t=delta;q=uniform,b=4,g=32;c=none", "t=delta;q=uniform,b=3,g=64;c=entropy"):
+        codec = KVCodec(sid, (L, H, T, C))
+        blob = codec.encode(kv)
+        flat = codec.decode(blob)
+        P = 32
+        npages = T // P + 2
+        table = torch.randperm(npages, device="cuda")[: T // P].to(torch.int32)
+        pages = torch.zeros(L * npages * P * H * C, dtype=torch.bfloat16, device="cuda")
+        codec.decode_paged(blob, pages, table, P, npages * P * H * C)
+        codec.check(decoding=True)
+        pv = pages.view(L, npages, P, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
+        assert torch.equal(pv, flat), sid
