@@ -220,21 +220,36 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   LModel<W> m;
   m.init(lsm, threadIdx.x);
   uint8_t* dst = a.packed_out + st.byte_off[si] + start * W / 8;
+  // symbols collect in a 64-bit accumulator and leave as big-endian 32-bit
+  // words when the destination is word aligned (blocks of a multiple of 32
+  // symbols are), else byte by byte
+  const bool word_out = (reinterpret_cast<uintptr_t>(dst) & 3u) == 0;
   uint64_t acc = 0;
   int nacc = 0, nout = 0;
   for (int i = 0; i < n; ++i) {
+    const unsigned mask = __activemask();
     const uint32_t unit = (i < H) ? div_recip(d.range, m.total, __ldg(magic + i)) : d.range / m.total;
     // code < low only in a malformed stream; offset() reads 0 -> symbol 0
     uint32_t plo, phi;
     const uint32_t s = m.find_scaled(d.offset(), unit, plo, phi);
-    d.advance(plo, phi);
+    d.advance_warp(plo, phi, mask);
     m.bump(s);
     acc = (acc << W) | s;
     nacc += W;
-    if (nacc >= 8) {
+    if (word_out) {
+      if (nacc >= 32) {
+        nacc -= 32;
+        *reinterpret_cast<uint32_t*>(dst + nout) = __byte_perm((uint32_t)(acc >> nacc), 0, 0x0123);
+        nout += 4;
+      }
+    } else if (nacc >= 8) {
       nacc -= 8;
       dst[nout++] = (uint8_t)(acc >> nacc);
     }
+  }
+  while (nacc >= 8) {  // whole bytes left over (word_out with a ragged tail)
+    nacc -= 8;
+    dst[nout++] = (uint8_t)(acc >> nacc);
   }
   // bytes consumed = 4 header + 4 priming + pulled (codecs.py:283-288)
   if ((int64_t)d.pulled() + 8 > len) atomicOr(a.status, KVC_FLAG_CODEC);
