@@ -237,6 +237,7 @@ __device__ __forceinline__ void tok_encode_groups(const FusedArgs& a, const uint
 #pragma unroll 1
   for (int gi = 0; gi < ngr; ++gi) {
     const unsigned mask = FULL ? 0xffffffffu : __activemask();
+    if constexpr (FULL) __syncwarp();  // proves convergence: no BRA.DIV before each vote
     uint32_t wv[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {

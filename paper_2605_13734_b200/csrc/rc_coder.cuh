@@ -10,6 +10,16 @@
 // because shifting a carry-free pair keeps it carry-free.  Those k bytes move
 // in one step; only the rare underflow case (top bytes differ but range <
 // BOTTOM, codecs.py:258-259) falls back to the reference's byte loop.
+//
+// The carry test is implicit.  Every reachable state has low + range <= 2^32
+// (true initially; an encode step stays inside the interval; a settled shift
+// leaves low + range < 2^32; the underflow fix rounds low + range up to a
+// multiple of 2^16).  So a carry means low + range == 2^32 exactly, i.e. t = 0
+// and x = low ^ t = low; that state is only entered through the underflow
+// loop, which leaves range < 2^24, so low > 2^32 - 2^24 has a set top bit and
+// clz(x) = 0: no bytes settle, as the reference decides.  (x = 0 would need
+// range = 0, which the underflow fix cannot produce: it only runs when the
+// interval crosses a multiple of 2^24, so low is not a multiple of 2^16.)
 #pragma once
 #include <stdint.h>
 
@@ -25,12 +35,12 @@ __device__ __forceinline__ uint32_t rc_clz(uint32_t x) {  // x != 0
 }
 
 // 8 * (number of settled leading bytes): 0, 8, 16 or 24 (branch-free: the
-// compiler would otherwise branch around the bit scan)
+// compiler would otherwise branch around the bit scan; no carry select, see
+// above)
 __device__ __forceinline__ uint32_t rc_settled_shift(uint32_t low, uint32_t range) {
   uint32_t sh;
-  asm("{\n\t.reg .u32 t, x, c;\n\t.reg .pred p;\n\t"
-      "add.u32 t, %1, %2;\n\txor.b32 x, %1, t;\n\tbfind.shiftamt.u32 c, x;\n\tand.b32 c, c, 24;\n\t"
-      "setp.lt.u32 p, t, %1;\n\tselp.u32 %0, 0, c, p;\n\t}"
+  asm("{\n\t.reg .u32 t, x, c;\n\t"
+      "add.u32 t, %1, %2;\n\txor.b32 x, %1, t;\n\tbfind.shiftamt.u32 c, x;\n\tand.b32 %0, c, 24;\n\t}"
       : "=r"(sh)
       : "r"(low), "r"(range));
   return sh;
@@ -68,7 +78,7 @@ struct RcEnc {
   // outgoing bytes in one IMAD.WIDE)
   __device__ __forceinline__ void put_mul(uint32_t sh) {
     uint32_t p;
-    asm("shl.b32 %0, 1, %1;" : "=r"(p) : "r"(sh));  // opaque: keep the multiplies
+    asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(p) : "r"(sh));  // 2^sh in one instruction; opaque: keep the multiplies
     const uint64_t lw = (uint64_t)low * p;
     whi = __funnelshift_l(wlo, whi, sh);
     wlo = wlo * p + (uint32_t)(lw >> 32);
@@ -124,29 +134,29 @@ struct RcEnc {
   }
 };
 
-// Decoder: input bytes come from a 64-bit window (next byte at the top of
-// hi) refilled one aligned word at a time; reads are clamped to the block's
-// last word and an overrun shows up as pulled > available.
+// Decoder.  `code` is always the four stream bytes after the ones consumed
+// (codecs.py:280-281, 303-305 shift one byte in per step), so it is not kept:
+// it is read out of two cached big-endian stream words w0:w1 at bit offset
+// pos (one funnel shift), and consuming bytes only advances pos.  When pos
+// passes a word boundary the words rotate and the next word (prefetched one
+// rotation ahead) comes in.  Reads are clamped to the block's last word; an
+// overrun shows up as pulled() > available.
 struct RcDec {
-  uint32_t low, range, code;
-  uint32_t hi, lo;
-  uint32_t avail;  // bytes in the window; >= 4 between symbols
+  uint32_t low, range;
+  uint32_t w0, w1;  // stream words wi-2, wi-1 (big-endian values)
+  uint32_t nxt;     // raw word wi, loaded one rotation ahead
+  uint32_t pos;     // bit offset of code's first byte in w0: 0..31 between steps
   uint32_t wi, wlast, skip;
-  uint32_t nxt;  // word wi, loaded one refill ahead so its latency is hidden
   const uint32_t* words;
 
-  __device__ __forceinline__ uint32_t load() {
-    const uint32_t w = __byte_perm(nxt, 0, 0x0123);
-    ++wi;
-    nxt = __ldg(words + min(wi, wlast));
-    return w;
-  }
-  __device__ __forceinline__ void refill() {
-    if (avail < 4u) {  // avail in 1..3 here
-      const uint32_t w = load();
-      hi |= w >> (8u * avail);
-      lo = w << (32u - 8u * avail);
-      avail += 4u;
+  __device__ __forceinline__ uint32_t code() const { return __funnelshift_l(w1, w0, pos); }
+  __device__ __forceinline__ void rotate() {  // at most one per step: pos < 32 + 24
+    if (pos >= 32u) {
+      w0 = w1;
+      w1 = __byte_perm(nxt, 0, 0x0123);
+      ++wi;
+      nxt = __ldg(words + min(wi, wlast));
+      pos -= 32u;
     }
   }
   // block = [BE32 length][range-coded bytes]; bytes [o0, o1) of the payload
@@ -156,55 +166,33 @@ struct RcDec {
     words = reinterpret_cast<const uint32_t*>(base);
     wlast = (uint32_t)((last - base) >> 2);
     skip = (uint32_t)(reinterpret_cast<uintptr_t>(blk + 4) - base);  // 0..3
-    wi = 0;
-    nxt = __ldg(words);
-    hi = load() << (8u * skip);
-    const uint32_t w1 = load();
-    if (skip == 0) {
-      lo = w1;
-      avail = 8u;
-    } else {
-      hi |= w1 >> (32u - 8u * skip);
-      lo = w1 << (8u * skip);
-      avail = 8u - skip;
-    }
-    // the first four bytes prime `code` (codecs.py:280-281)
-    code = hi;
-    hi = lo;
-    lo = 0;
-    avail -= 4u;  // 1..4
-    refill();
+    w0 = __byte_perm(__ldg(words), 0, 0x0123);
+    w1 = __byte_perm(__ldg(words + min(1u, wlast)), 0, 0x0123);
+    nxt = __ldg(words + min(2u, wlast));
+    wi = 2;
+    pos = 8u * skip;  // the first four bytes prime code
     low = 0;
     range = 0xFFFFFFFFu;
   }
-  // pull sh/8 <= 3 bytes into code (codecs.py:303-305, once per byte)
+  // consume sh/8 <= 3 bytes (codecs.py:303-305, once per byte)
   __device__ __forceinline__ void take_sh(uint32_t sh) {
-    code = (code << sh) | __funnelshift_l(hi, 0u, sh);
-    hi = __funnelshift_l(lo, hi, sh);
-    lo <<= sh;
-    avail -= sh >> 3;
+    pos += sh;
+    rotate();
     low <<= sh;
     range <<= sh;
-    refill();
   }
   __device__ __forceinline__ void take(uint32_t k) { take_sh(8u * k); }
-  // take_sh with the shifts as multiplies by p = 2^sh (FMA pipe; see
-  // RcEnc::put_mul): hi * p yields the shifted window word and the bytes
-  // entering `code` in one IMAD.WIDE
+  // take_sh with the low / range shifts as multiplies by p = 2^sh (FMA pipe)
   __device__ __forceinline__ void take_mul(uint32_t sh) {
     uint32_t p;
-    asm("shl.b32 %0, 1, %1;" : "=r"(p) : "r"(sh));
-    const uint64_t hw = (uint64_t)hi * p, lw = (uint64_t)lo * p;
-    code = code * p + (uint32_t)(hw >> 32);
-    hi = (uint32_t)hw + (uint32_t)(lw >> 32);
-    lo = (uint32_t)lw;
-    avail -= sh >> 3;
+    asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(p) : "r"(sh));  // 2^sh
     low *= p;
     range *= p;
-    refill();
+    pos += sh;
+    rotate();
   }
   // stream bytes consumed after the 4 priming bytes
-  __device__ __forceinline__ uint32_t pulled() const { return 4u * wi - skip - 4u - avail; }
+  __device__ __forceinline__ uint32_t pulled() const { return 4u * (wi - 2u) + (pos >> 3) - skip; }
   __device__ __forceinline__ void underflow() {
     for (;;) {
       const uint32_t t = low + range;
@@ -216,7 +204,10 @@ struct RcDec {
     }
   }
   // code - low (codecs.py:290-292); a malformed stream with code < low reads 0
-  __device__ __forceinline__ uint32_t offset() const { return code >= low ? code - low : 0u; }
+  __device__ __forceinline__ uint32_t offset() const {
+    const uint32_t c = code();
+    return c >= low ? c - low : 0u;
+  }
   __device__ __forceinline__ void advance(uint32_t plo, uint32_t phi) {  // plo = unit*cum, phi = unit*(cum+freq)
     low += plo;
     range = phi - plo;

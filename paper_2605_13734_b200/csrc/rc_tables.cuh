@@ -19,8 +19,14 @@ const uint32_t* recip_tables(cudaStream_t s);
 
 __device__ __forceinline__ uint32_t div_recip(uint32_t n, uint32_t d, uint32_t m) {
   // floor(n / d) given m = floor(2^32 / d): the product estimate is q or q-1
-  const uint32_t q = __umulhi(n, m);
-  return q + ((n - q * d) >= d ? 1u : 0u);
+  // (PTX: the compiler's form of the correction costs two more instructions)
+  uint32_t q;
+  asm("{\n\t.reg .u32 r, nd;\n\t.reg .pred p;\n\t"
+      "mul.hi.u32 %0, %1, %3;\n\tneg.s32 nd, %2;\n\tmad.lo.u32 r, %0, nd, %1;\n\t"
+      "setp.ge.u32 p, r, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "=&r"(q)
+      : "r"(n), "r"(d), "r"(m));
+  return q;
 }
 
 }  // namespace kvc
