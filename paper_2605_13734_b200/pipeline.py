@@ -179,6 +179,7 @@ class WallClockTimer:
         durations = []
         result = None
         for _ in range(self.repeats):
+            result = None
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             result = fn()
@@ -229,6 +230,7 @@ class CudaEventTimer:
         for _ in range(self.repeats):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            result = None  # free the previous result first: its allocation is reused, not grown
             a.record()
             result = fn()
             b.record()
