@@ -125,8 +125,9 @@ __device__ __forceinline__ void pack32_dispatch(int w, const float* q, uint8_t* 
   }
 }
 
-// Unpack 32 symbols of width W from src (4-byte aligned) into floats.
-template <int W>
+// Unpack 32 symbols of width W from src (4-byte aligned) into floats
+// (RAW: the magic floats 2^23 + symbol, the 2^23 removed by the caller).
+template <int W, bool RAW = false>
 __device__ __forceinline__ void unpack32(const uint8_t* src, float* v) {
   uint32_t be[W];
   if constexpr (W % 4 == 0) {
@@ -156,22 +157,44 @@ __device__ __forceinline__ void unpack32(const uint8_t* src, float* v) {
     } else {
       s = ((be[k] << (off + W - 32)) | (be[k + 1] >> (64 - off - W))) & ((1u << W) - 1u);
     }
-    v[i] = __uint_as_float(0x4B000000u | s) - 8388608.0f;
+    v[i] = RAW ? __uint_as_float(0x4B000000u | s) : __uint_as_float(0x4B000000u | s) - 8388608.0f;
   }
 }
 
+template <bool RAW = false>
 __device__ __forceinline__ void unpack32_dispatch(int w, const uint8_t* src, float* v) {
   switch (w) {
-    case 1: unpack32<1>(src, v); break;
-    case 2: unpack32<2>(src, v); break;
-    case 3: unpack32<3>(src, v); break;
-    case 4: unpack32<4>(src, v); break;
-    case 5: unpack32<5>(src, v); break;
-    case 6: unpack32<6>(src, v); break;
-    case 7: unpack32<7>(src, v); break;
-    default: unpack32<8>(src, v); break;
+    case 1: unpack32<1, RAW>(src, v); break;
+    case 2: unpack32<2, RAW>(src, v); break;
+    case 3: unpack32<3, RAW>(src, v); break;
+    case 4: unpack32<4, RAW>(src, v); break;
+    case 5: unpack32<5, RAW>(src, v); break;
+    case 6: unpack32<6, RAW>(src, v); break;
+    case 7: unpack32<7, RAW>(src, v); break;
+    default: unpack32<8, RAW>(src, v); break;
   }
 }
+
+// packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2: two IEEE round-to-nearest
+// operations per instruction, lane-wise identical to the scalar ones).  PTX
+// with an explicit .rn: never contracted into an FFMA2 (the __fadd2_rn /
+// __fmul2_rn intrinsics are, which would break quantize.py:178's unfused
+// multiply-then-add).
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+#define KVC_F2OP(name, op)                                                                               \
+  __device__ __forceinline__ float2 name(float2 a, float2 b) {                                          \
+    float2 d;                                                                                            \
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t" op      \
+        " rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"                                                  \
+        : "=f"(d.x), "=f"(d.y)                                                                           \
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));                                                      \
+    return d;                                                                                            \
+  }
+KVC_F2OP(f2add, "add.rn.f32x2")
+KVC_F2OP(f2mul, "mul.rn.f32x2")
+#undef KVC_F2OP
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) { return f2add(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
 // ------------------------------------------------------------ group stats
 // min / max of 32 fp32 values
@@ -271,11 +294,15 @@ __device__ __forceinline__ void quantize64(float* y, float mn0, float mx0, float
         easy = l1 >= -0.5f && h1 < q.lv + 0.5f;
       }
       if (__all_sync(0xffffffffu, easy)) {
+        // two values per FADD2 / FMUL2 / FFMA2, the same roundings as the
+        // scalar sequence of quant_magic (minus the clip)
+        float2* y2 = reinterpret_cast<float2*>(yy);
+        const float2 nz = f2(-q.z, -q.z), r2 = f2(q.r, q.r), ns = f2(-q.s, -q.s), mg = f2(kMagicRound, kMagicRound);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float d = __fsub_rn(yy[i], q.z);
-          const float q0 = __fmul_rn(d, q.r);
-          yy[i] = __fadd_rn(__fmaf_rn(__fmaf_rn(-q0, q.s, d), q.r, q0), kMagicRound);
+        for (int i = 0; i < 16; ++i) {
+          const float2 d = f2add(y2[i], nz);
+          const float2 q0 = f2mul(d, r2);
+          y2[i] = f2add(f2fma(f2fma(q0, ns, d), r2, q0), mg);
         }
       } else if (q.mode == 0) {
 #pragma unroll
@@ -365,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     // invalid tail rows run the same code (shuffles need the full warp) but
     // store nothing
 
-    float y[64];
+    __align__(8) float y[64];
     int cb0, cb1;
     bool hadlayout = false;
     bool need_fix = false;  // Hadamard: this row is re-encoded exactly by k_encode_fixup
@@ -401,42 +428,53 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
         f[2 * j] = f32bits_scaled_f64(wv[j] << 16);
         f[2 * j + 1] = f32bits_scaled_f64(wv[j] & 0xFFFF0000u);
       }
-      // stages h = 1..32 (transforms.py:41-46 order), in registers
+      // stages h = 1..32 (transforms.py:41-46 order), in registers.  At h = 32
+      // thread B (half 1) writes its two outputs swapped (u - v at i, u + v at
+      // i + 32; the same roundings, as one DFMA with -1 each), so afterwards
+      // both threads hold the value the partner needs at local 32 + k and the
+      // one they keep at local k: the h = 64 exchange below needs no selects.
+      const double sgn = half ? -1.0 : 1.0;
 #pragma unroll
       for (int h = 1; h < 64; h <<= 1) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
           if ((i & h) == 0) {
             const double u = f[i], v = f[i + h];
-            f[i] = u + v;
-            f[i + h] = u - v;
+            if (h == 32) {
+              f[i] = __fma_rn(v, sgn, u);
+              f[i + h] = __fma_rn(v, -sgn, u);
+            } else {
+              f[i] = u + v;
+              f[i + h] = u - v;
+            }
           }
         }
       }
       // stage h = 64 across the thread pair: A (half 0) keeps outputs 0..31 and
-      // 64..95, B keeps 32..63 and 96..127.
+      // 64..95, B keeps 32..63 and 96..127.  A's local k / 32 + k hold its
+      // T[k] / T[32 + k]; B's hold T[32 + k] / T[k].  Each sends local 32 + k
+      // and forms (own + r, own - r): A gets out[k], out[64 + k]; B gets
+      // out[32 + k] (a + b = b + a) and -out[96 + k] (own - r = -(r - own),
+      // negated back through the sign of the scale below).
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const double send = half ? f[k] : f[32 + k];
+        const double send = f[32 + k];
         const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(send), 1);
         const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(send), 1);
         const double r = __hiloint2double(hi, lo);
-        if (!half) {
-          const double u = f[k];
-          f[k] = u + r;
-          f[32 + k] = u - r;
-        } else {
-          const double v = f[32 + k];
-          f[k] = r + v;
-          f[32 + k] = r - v;
-        }
+        const double u = f[k];
+        f[k] = u + r;
+        f[32 + k] = u - r;
       }
       // RN32(RN64(S / sqrt n)) as one F2F of RN64(S * RN64(1/sqrt n)); the two
-      // differ only within 4 ulp64 of an f32 rounding midpoint (numerics.cuh)
+      // differ only within 4 ulp64 of an f32 rounding midpoint (numerics.cuh).
+      // B's second half is scaled by -hk (RN is sign-symmetric; an exact zero
+      // comes out as -0 there, made +0 in the group min / max below).
+      const double hk2 = half ? -a.hk : a.hk;
       bool mid = false;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        const double q = f[i] * a.hk;
+        const double q = f[i] * (i < 32 ? a.hk : hk2);
         mid |= ((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x0FFFFFFCu <= 8u;
         y[i] = __double2float_rn(q);
       }
@@ -495,6 +533,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     } else {
       minmax32(y, mn0, mx0);
       minmax32(y + 32, mn1, mx1);
+      if (MODE == M_HADAMARD) {  // -0 from the negated half -> +0 (x + 0 = x otherwise)
+        mn1 = __fadd_rn(mn1, 0.0f);
+        mx1 = __fadd_rn(mx1, 0.0f);
+      }
     }
 
     int w;
@@ -521,39 +563,113 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
 }
 
 // ------------------------------------------------------------ decode kernel
-// zero + symbol*scale (quantize.py:178) for the thread's 64 values, unfused
-// like the reference.  (FOLD = 1/sqrt(128) folded into scale and zero, one
-// FMA per value: measured 3% faster but it breaks the 1-bf16-ulp bound on
-// near-zero outputs, so the decode does not use it.)  Returns false if a group's scale or zero is not finite -- the only
-// way a dequantized or Hadamard-mixed value can be non-finite (|z|, s <=
-// 65504, symbols <= 255: no fp32 overflow).
-template <int G, bool FOLD>
-__device__ __forceinline__ bool dequant64(float* y, int cb0, int cb1, int64_t row, const __half* scales,
-                                          const __half* zeros) {
-  bool finite = true;
+// Dequantize + inverse transform of the thread's 64 values (hadamard layout:
+// chunks at channels 32*half and 64 + 32*half; natural: 64*half, +32), one
+// group per 32-value chunk (G >= 32).  y holds the magic floats 2^23 + symbol.
+// zero + symbol * scale (quantize.py:178) is one FFMA2 per two values: the
+// product of a symbol (<= 8 bits) and an fp16 scale (11-bit significand) is
+// exact in fp32, so the fused and the reference's separate multiply and add
+// round identically.  Returns false if a group's scale or zero is not finite
+// -- the only way a dequantized or Hadamard-mixed value can be non-finite.
+template <int MODE, int G>
+__device__ __forceinline__ bool dec_core(float* y, const float* sc, const float* zr, int half, int64_t lh,
+                                         const DecArgs& a) {
+  static_assert(G >= 32, "fast path groups");
+  const Geo& g = a.g;
+  bool groups_finite = true;
+  float2* Y = reinterpret_cast<float2*>(y);
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
-    const int cb = c ? cb1 : cb0;
+    groups_finite &= isfinite(sc[c]) && isfinite(zr[c]);
+    const float2 s2 = f2(sc[c], sc[c]), z2 = f2(zr[c], zr[c]), m2 = f2(-8388608.0f, -8388608.0f);
 #pragma unroll
-    for (int j = 0; j < (G < 32 ? 32 / G : 1); ++j) {
-      const int64_t gi = row * (128 / G) + (cb + j * G) / G;
-      float s = __half2float(scales[gi]), z = __half2float(zeros[gi]);
-      finite &= isfinite(s) && isfinite(z);
-      constexpr int n = G < 32 ? G : 32;
-      if (FOLD) {
-        s = __fmul_rn(s, 0.08838834764831845f);  // RN32(1/sqrt(128))
-        z = __fmul_rn(z, 0.08838834764831845f);
-#pragma unroll
-        for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fmaf_rn(y[32 * c + j * n + i], s, z);
-      } else {
-#pragma unroll
-        for (int i = 0; i < n; ++i) y[32 * c + j * n + i] = __fadd_rn(z, __fmul_rn(y[32 * c + j * n + i], s));
-      }
+    for (int i = 0; i < 16; ++i) {
+      float2& v = Y[16 * c + i];
+      v = f2fma(f2add(v, m2), s2, z2);
     }
   }
-  return finite;
+  if (MODE == M_HADAMARD) {
+    // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
+    // (decode is held to tolerance), two values per FADD2: in-thread stages
+    // over channel bits 0-4 and 6, one pair exchange for bit 5.  At the
+    // bit-6 stage B (half 1) writes its outputs swapped (one FFMA2 by -1 each,
+    // same roundings) so both threads send local 32 + k and keep local k.
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {  // h = 1: the two lanes of one pair
+      const float u = Y[i].x, v = Y[i].y;
+      Y[i] = f2(u + v, u - v);
+    }
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1) {  // h = 2..16 in float2 units
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if ((i & h) == 0) {
+          const float2 u = Y[i], v = Y[i + h];
+          Y[i] = f2add(u, v);
+          Y[i + h] = f2sub(u, v);
+        }
+      }
+    }
+    const float sg = half ? -1.0f : 1.0f;
+    const float2 sp = f2(sg, sg), sn = f2(-sg, -sg);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 u = Y[i], v = Y[16 + i];
+      Y[i] = f2fma(v, sp, u);
+      Y[16 + i] = f2fma(v, sn, u);
+    }
+    // A: local k = channel k, 32 + k = channel 32 + k; B: local k = channel
+    // 64 + k, 32 + k = -(channel 96 + k) (own - r = -(r - own)), restored by
+    // the sign of the final scale
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float2 send = Y[16 + k];
+      const float2 r = f2(__shfl_xor_sync(0xffffffffu, send.x, 1), __shfl_xor_sync(0xffffffffu, send.y, 1));
+      const float2 u = Y[k];
+      Y[k] = f2add(u, r);
+      Y[16 + k] = f2sub(u, r);
+    }
+    const float c = 0.08838834764831845f;  // RN32(1/sqrt(128))
+    const float2 c0 = f2(c, c), c1 = half ? f2(-c, -c) : c0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      Y[i] = f2mul(Y[i], c0);
+      Y[16 + i] = f2mul(Y[16 + i], c1);
+    }
+  } else if (MODE == M_AFFINE) {
+    const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
+    const __half* scl = mu + g.LH * 128;
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
+  }
+  return groups_finite;
 }
 
+// bf16-pack 8 values
+__device__ __forceinline__ uint4 pack_bf16x8(const float* y) {
+  uint32_t p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
+    p[q] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
+template <int MODE>
+__device__ __forceinline__ void dec_flags(const float* y, bool groups_finite, uint32_t& flags) {
+  if (MODE == M_AFFINE) {  // y * (1/a) + mu can overflow for a tiny fp16 a
+    float chk = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
+    if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+  } else if (!groups_finite) {
+    flags |= KVC_FLAG_NONFINITE_TRANSFORM;
+  }
+}
+
+// Direct decode: any width layout, contiguous or paged output, bf16 or fp32.
 template <int MODE, typename Tout, int G, int W>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
   const Geo& g = a.g;
@@ -588,82 +704,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
         asm volatile("prefetch.global.L1 [%0];" ::"l"(zeros + nrow * (128 / G)));
       }
     }
-    float y[64];
+    __align__(8) float y[64];
     if constexpr (W == 0) {
-      unpack32_dispatch(w, src + cb0 * w / 8, y);
-      unpack32_dispatch(w, src + cb1 * w / 8, y + 32);
+      unpack32_dispatch<true>(w, src + cb0 * w / 8, y);
+      unpack32_dispatch<true>(w, src + cb1 * w / 8, y + 32);
     } else {
-      unpack32<W>(src + cb0 * W / 8, y);
-      unpack32<W>(src + cb1 * W / 8, y + 32);
+      unpack32<W, true>(src + cb0 * W / 8, y);
+      unpack32<W, true>(src + cb1 * W / 8, y + 32);
     }
-    const bool groups_finite = dequant64<G, false>(y, cb0, cb1, row, scales, zeros);
-    if (MODE == M_HADAMARD) {
-      // inverse = the same orthonormal WHT (transforms.py:73-75), in fp32
-      // (decode is held to tolerance): in-thread stages over channel bits
-      // 0-4 and 6, one pair exchange for bit 5.
-#pragma unroll
-      for (int h = 1; h < 32; h <<= 1) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          if ((i & h) == 0) {
-            const float u = y[i], v = y[i + h];
-            y[i] = u + v;
-            y[i + h] = u - v;
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float u = y[i], v = y[32 + i];
-        y[i] = u + v;
-        y[32 + i] = u - v;
-      }
-      // afterwards A (half 0) holds channels 0..63 and B 64..127
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float send = half ? y[k] : y[32 + k];
-        const float r = __shfl_xor_sync(0xffffffffu, send, 1);
-        if (!half) {
-          const float u = y[k];
-          y[k] = u + r;
-          y[32 + k] = u - r;
-        } else {
-          const float v = y[32 + k];
-          y[k] = r + v;
-          y[32 + k] = r - v;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 64; ++i) y[i] = __fmul_rn(y[i], 0.08838834764831845f);  // RN32(1/sqrt(128))
-    } else if (MODE == M_AFFINE) {
-      const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
-      const __half* scl = mu + g.LH * 128;
-#pragma unroll
-      for (int i = 0; i < 64; ++i)
-        y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
-    }
+    const int64_t gi0 = row * (128 / G) + cb0 / G, gi1 = row * (128 / G) + cb1 / G;
+    const float sc[2] = {__half2float(scales[gi0]), __half2float(scales[gi1])};
+    const float zr[2] = {__half2float(zeros[gi0]), __half2float(zeros[gi1])};
+    const bool groups_finite = dec_core<MODE, G>(y, sc, zr, half, lh, a);
     if (!valid) continue;
-    if (MODE == M_AFFINE) {  // y * (1/a) + mu can overflow for a tiny fp16 a
-      float chk = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) chk = __fmaf_rn(y[i], 0.0f, chk);
-      if (chk != 0.0f) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
-    } else if (!groups_finite) {
-      flags |= KVC_FLAG_NONFINITE_TRANSFORM;
-    }
+    dec_flags<MODE>(y, groups_finite, flags);
     Tout* out = reinterpret_cast<Tout*>(a.out) + out_index(a, lh, t, 64 * half);
     if constexpr (sizeof(Tout) == 2) {
       uint4* o = reinterpret_cast<uint4*>(out);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        uint32_t p[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          __nv_bfloat162 b = __floats2bfloat162_rn(y[8 * k + 2 * q], y[8 * k + 2 * q + 1]);
-          p[q] = *reinterpret_cast<uint32_t*>(&b);
-        }
-        o[k] = make_uint4(p[0], p[1], p[2], p[3]);
-      }
+      for (int k = 0; k < 8; ++k) o[k] = pack_bf16x8(y + 8 * k);
     } else {
       float4* o = reinterpret_cast<float4*>(out);
 #pragma unroll
@@ -671,6 +730,126 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
     }
   }
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
+}
+
+// Staged decode (uniform width, contiguous bf16 output): per 64-row tile the
+// packed rows (1024*W B), scales and zeros (each 64*(128/G)*2 B) are
+// contiguous, so three 1-D bulk copies (cp.async.bulk, mbarrier completion)
+// fill an NS-deep ring; the tile's 16 KB of bf16 rows is written to shared
+// memory in the 128B-swizzled TMA layout (conflict-free 16 B stores) and
+// leaves as one tensor store (double-buffered, bulk_group).  The partial last
+// tile reads its inputs directly; the tensor store clips rows past the end.
+constexpr int kDecStages = 3;
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int W, int G>
+__host__ __device__ constexpr int dec_stage_bytes() {
+  return 1024 * W + 2 * (64 * (128 / G) * 2);
+}
+template <int W, int G>
+__host__ __device__ constexpr int dec_smem_bytes() {
+  return 2 * kTileBytes + kDecStages * dec_stage_bytes<W, G>() + 1024 + 64;
+}
+
+template <int MODE, int G, int W>
+__global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__ CUtensorMap omap, const DecArgs a) {
+  constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<W, G>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* obuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ibuf = obuf + 2 * kTileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ibuf + kDecStages * STAGE);
+  const Geo& g = a.g;
+  const int64_t nrows = g.LH * g.T;
+  const int64_t ntiles = (nrows + kRows - 1) / kRows, nfull = nrows / kRows;
+  const int tid = threadIdx.x, half = tid & 1, lr = tid >> 1;
+  const uint32_t sw = (uint32_t)(tid & 7);
+  const __half* scales = reinterpret_cast<const __half*>(a.meta);
+  const __half* zeros = scales + g.ngroups;
+  constexpr bool had = MODE == M_HADAMARD;
+  const int cb0 = had ? 32 * half : 64 * half;
+  const int cb1 = had ? 64 + 32 * half : 64 * half + 32;
+  auto issue = [&](int s, int64_t tile) {
+    uint8_t* d = ibuf + s * STAGE;
+    mbar_expect_tx(&full[s], STAGE);
+    bulk_g2s(d, a.packed + tile * PK, PK, &full[s]);
+    bulk_g2s(d + PK, scales + tile * (SB / 2), SB, &full[s]);
+    bulk_g2s(d + PK + SB, zeros + tile * (SB / 2), SB, &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kDecStages; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < nfull) issue(s, tile);
+    }
+  }
+  uint32_t flags = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % kDecStages;
+    const int64_t row0 = tile * kRows + lr;
+    const bool valid = row0 < nrows;
+    const int64_t row = valid ? row0 : nrows - 1;
+    const int64_t lh = row / g.T;
+    __align__(8) float y[64];
+    float sc[2], zr[2];
+    if (tile < nfull) {
+      mbar_wait(&full[s], (uint32_t)((it / kDecStages) & 1));
+      const uint8_t* st = ibuf + s * STAGE;
+      unpack32<W, true>(st + lr * 16 * W + cb0 * W / 8, y);
+      unpack32<W, true>(st + lr * 16 * W + cb1 * W / 8, y + 32);
+      const __half* ss = reinterpret_cast<const __half*>(st + PK) + lr * (128 / G);
+      const __half* zz = reinterpret_cast<const __half*>(st + PK + SB) + lr * (128 / G);
+      sc[0] = __half2float(ss[cb0 / G]);
+      sc[1] = __half2float(ss[cb1 / G]);
+      zr[0] = __half2float(zz[cb0 / G]);
+      zr[1] = __half2float(zz[cb1 / G]);
+    } else {  // the partial last tile
+      const uint8_t* src = a.packed + row * 16 * W;
+      unpack32<W, true>(src + cb0 * W / 8, y);
+      unpack32<W, true>(src + cb1 * W / 8, y + 32);
+      const int64_t gi0 = row * (128 / G) + cb0 / G, gi1 = row * (128 / G) + cb1 / G;
+      sc[0] = __half2float(scales[gi0]);
+      sc[1] = __half2float(scales[gi1]);
+      zr[0] = __half2float(zeros[gi0]);
+      zr[1] = __half2float(zeros[gi1]);
+    }
+    // the output buffer written two tiles ago must have been read out
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();  // stage s consumed by every thread; obuf[it & 1] free
+    if (tid == 0) {
+      const int64_t next = tile + (int64_t)kDecStages * gridDim.x;
+      if (next < nfull) {
+        fence_proxy_async();
+        issue(s, next);
+      }
+    }
+    const bool groups_finite = dec_core<MODE, G>(y, sc, zr, half, lh, a);
+    if (valid) dec_flags<MODE>(y, groups_finite, flags);
+    uint8_t* ob = obuf + (it & 1) * kTileBytes + tid * 128;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) *reinterpret_cast<uint4*>(ob + (((uint32_t)k ^ sw) << 4)) = pack_bf16x8(y + 8 * k);
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) tma_store_2d(&omap, obuf + (it & 1) * kTileBytes, 0, (int)(tile * kThreads));
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
@@ -737,8 +916,35 @@ cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count,
   }
 }
 
+// the staged kernel needs a contiguous bf16 output and 16-byte aligned tile
+// bases for the bulk copies (packed rows, scales, zeros)
+template <typename Tout, int W>
+bool dec_staged_ok(const DecArgs& a) {
+  if (sizeof(Tout) != 2 || W == 0 || a.paged) return false;
+  const int64_t nrows = a.g.LH * a.g.T;
+  if (2 * nrows >= (1ll << 31)) return false;
+  const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  return al(a.packed) && al(a.meta) && al(a.out) && (a.g.ngroups % 8) == 0;
+}
+
 template <int MODE, typename Tout, int G, int W>
 cudaError_t launch_dec_gw(const DecArgs& a, int sm_count, cudaStream_t s) {
+  if constexpr (sizeof(Tout) == 2 && W != 0) {
+    CUtensorMap omap;
+    if (dec_staged_ok<Tout, W>(a) && make_input_map(&omap, a.out, a.g.LH * a.g.T)) {
+      auto k = k_dec128r<MODE, G, W>;
+      constexpr int smem = dec_smem_bytes<W, G>();
+      set_max_dyn_smem<k_dec128r<MODE, G, W>>(smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
+      if (per_sm < 1) per_sm = 1;
+      const int64_t need = (a.g.LH * a.g.T + kRows - 1) / kRows;
+      int64_t grid = (int64_t)sm_count * per_sm;
+      if (grid > need) grid = need;
+      k<<<(unsigned)grid, kThreads, smem, s>>>(omap, a);
+      return cudaGetLastError();
+    }
+  }
   auto k = k_dec128<MODE, Tout, G, W>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);

@@ -438,3 +438,39 @@ def test_delta_chunked_decode_falls_back_when_sums_round():
     codec.check(decoding=True)
     rec = oracle.decode_blob(ref["payload"], ref["metadata"], None, sid, shape, block=1024)
     assert np.array_equal(out.view(np.uint32), rec.view(np.uint32))
+
+
+@pytest.mark.parametrize("sid", [
+    "t=hadamard;q=uniform,b=4,g=32;c=none",
+    "t=hadamard;q=uniform,b=2,g=64;c=none",
+    "t=identity;q=uniform,b=4,g=32;c=none",
+    "t=identity;q=uniform,b=8,g=128;c=none",
+    "t=affine;q=uniform,b=8,g=32;c=none",
+    "t=hadamard;q=uniform,b=2,g=32;c=entropy",
+])
+@pytest.mark.parametrize("shape", [(2, 4, 256, 128), (1, 2, 100, 128), (1, 1, 3, 128)])
+def test_staged_bf16_decode_matches_fp32_decode(sid, shape):
+    """Contiguous bf16 decode (the staged bulk-copy / tensor-store kernel for
+    uniform widths when the tile bases are 16-byte aligned; (1, 1, 3) has
+    12 groups and takes the direct kernel): equal to the fp32 decode rounded
+    to bf16, including the partial last tile, and within tolerance of the
+    oracle through that fp32 decode."""
+    from paper_2605_13734_b200 import KVCodec
+
+    v, _ = oracle.generate_kv(*shape, seed=11)
+    tb, vb = bf16_exact(v)
+    kv = tb.cuda().contiguous()
+    c32 = KVCodec(sid, shape, out_dtype=torch.float32)
+    c16 = KVCodec(sid, shape, out_dtype=torch.bfloat16)
+    blob = c32.encode(kv)
+    c32.check()
+    o32 = c32.decode(blob)
+    o16 = c16.decode(blob)
+    torch.cuda.synchronize()
+    c32.check(decoding=True)
+    c16.check(decoding=True)
+    assert o16.dtype == torch.bfloat16
+    assert torch.equal(o16.view(torch.int16), o32.to(torch.bfloat16).view(torch.int16)), sid
+    ref = oracle.encode_blob(vb, None, sid)
+    rec = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, shape)
+    assert_decoded(o32.cpu().numpy(), rec, sid, shape)

@@ -3,12 +3,18 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #define N_ITER 4096
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
+  unsigned long long d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
 template <int OP>
 __global__ void k(float* out, double* dout, int seed) {
   double a = threadIdx.x * 1.0000001 + seed, b = 1.0 + 1e-9 * seed, c = a * 0.5, d = a * 0.25;
   float fa = threadIdx.x * 1.01f, fb = fa * 0.5f, fc = fa * 0.25f, fd = fa * 0.125f;
   unsigned ua = threadIdx.x + 12345u, ub = ua * 7u + 1, uc = ua ^ 0x55u, ud = ua + 99u;
   unsigned dv = (seed & 0xFFFF) + 37;
+  float fe = fa * 3.f, ff = fa * 5.f, fg = fa * 7.f, fh = fa * 9.f;
+  unsigned long long ua2 = ua * 0x100000001ull, ub2 = ub * 0x100000001ull, uc2 = uc * 0x100000001ull, ud2 = ud * 0x100000001ull;
 #pragma unroll 16
   for (int i = 0; i < N_ITER; ++i) {
     if (OP == 0) { a = a + b; c = c + b; d = d + b; fa = fa + 1.0f; }                  // DADD x3 indep
@@ -24,9 +30,13 @@ __global__ void k(float* out, double* dout, int seed) {
     if (OP == 10) { ua = ua * 0x9E3779B9u + (ua >> 7); ub = ub * 0x9E3779B9u + (ub >> 7); uc = uc*0x9E3779B9u + (uc>>7); ud = ud*0x9E3779B9u+(ud>>7);} // IMAD+SHF
     if (OP == 11) { fa = __frcp_rn(fa + 1.0f); fb = __frcp_rn(fb + 1.0f);}                  // frcp_rn
     if (OP == 12) { a = __ddiv_rn(a, b + i); c = __ddiv_rn(c, b + i); }                     // DDIV
+    if (OP == 14) { ua2 = f2add(ua2, ub2); ub2 = f2add(ub2, uc2); uc2 = f2add(uc2, ud2); ud2 = f2add(ud2, ua2); }  // FADD2 (4 instr)
+    if (OP == 15) { a = __fma_rn(a, b, c); c = __fma_rn(c, b, d); d = __fma_rn(d, b, a); }  // DFMA x3
+    if (OP == 16) { ua2 = f2fma(ua2, ub2, uc2); ub2 = f2fma(ub2, uc2, ud2); uc2 = f2fma(uc2, ud2, ua2); ud2 = f2fma(ud2, ua2, ub2); }  // FFMA2
+    if (OP == 17) { fa = fa + fb; fb = fb + fc; fc = fc + fd; fd = fd + fa; fe = fe + ff; ff = ff + fg; fg = fg + fh; fh = fh + fe; }  // FADD x8, two chains
     if (OP == 13) { fa = __fdiv_rn(fa, fb + 1.0f); fb = __fdiv_rn(fb, fc + 2.0f); }         // FDIV
   }
-  if (a + c + d + fa + fb + fc + fd + ua + ub + uc + ud == 0.123) { out[0] = fa; dout[0] = a; }
+  if (a + c + d + fa + fb + fc + fd + fe + ff + fg + fh + ua + ub + uc + ud + (double)(ua2 ^ ub2 ^ uc2 ^ ud2) == 0.123) { out[0] = fa; dout[0] = a; }
 }
 template <int OP> float run(const char* name, int per_iter_ops, float* o, double* d) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -58,6 +68,10 @@ int main() {
   run<11>("frcp_rn x2", 2, o, d);
   run<12>("ddiv_rn x2", 2, o, d);
   run<13>("fdiv_rn x2", 2, o, d);
+  run<14>("FADD2 x4 (f32x2) dep-chain", 4, o, d);
+  run<15>("DFMA x3", 3, o, d);
+  run<16>("FFMA2 x4 (f32x2) dep-chain", 4, o, d);
+  run<17>("FADD x8 two chains", 8, o, d);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
