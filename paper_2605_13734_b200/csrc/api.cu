@@ -276,15 +276,6 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
     p.ws_fix = off;
     off = align_up(off + 16 + 4 * g.LH * g.T, 256);
   }
-  // large-alphabet entropy encode precomputes its model per batch of blocks
-  // (rc_large.cu): 4 bytes per symbol, batches of up to 2^18 blocks (enough
-  // coder threads to fill the GPU; at most 2 GB at 2048-symbol blocks)
-  p.model_blocks = 0;
-  p.ws_model = off;
-  if (g.codec == C_ENTROPY && wmax >= 5 && g.block <= 2048) {
-    p.model_blocks = std::min<int64_t>(p.max_blocks + 1, 1 << 18);
-    off = align_up(off + p.model_blocks * g.block * 4 + p.model_blocks * 4 + 16, 256);
-  }
   p.ws_bytes = off;
   snprintf(p.id, sizeof p.id, "%s", canon.c_str());
   int dev = 0;
@@ -440,11 +431,6 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
     c.slot_bytes = p.slot_bytes;
     c.max_blocks = p.max_blocks;
     c.status = status;
-    if (p.model_blocks > 0) {
-      c.model = reinterpret_cast<uint32_t*>(ws + p.ws_model);
-      c.model_total = c.model + p.model_blocks * g.block;
-      c.model_blocks = p.model_blocks;
-    }
     if ((e = launch_codec_encode(c, p.sm_count, s)) != cudaSuccess) return cuda_fail(e, "codec encode");
   }
   return KVC_OK;

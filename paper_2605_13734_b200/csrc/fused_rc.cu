@@ -68,6 +68,22 @@ __device__ __forceinline__ uint16_t half_at(uint2 v, int k) {
   const uint32_t w = (k & 2) ? v.y : v.x;
   return (uint16_t)(w >> (16 * (k & 1)));
 }
+// packed fp32x2 add / multiply in PTX with an explicit .rn (never contracted
+// into an FFMA2)
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -111,15 +127,18 @@ __device__ __forceinline__ void quant32(Val&& value, float mn, float mx, int w, 
     easy = quo(mn) >= -0.5f && quo(mx) < q.lv + 0.5f;
   }
   if (__all_sync(mask, easy)) {
+    // two values per FADD2 / FMUL2 / FFMA2 (lane-wise the scalar roundings)
+    const float2 nz = make_float2(-q.z, -q.z), r2 = make_float2(q.r, q.r), ns = make_float2(-q.s, -q.s);
+    const float2 mg = make_float2(kMagicRound, kMagicRound);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       uint32_t acc = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float d = __fsub_rn(value(8 * k + j), q.z);
-        const float q0 = __fmul_rn(d, q.r);
-        const float q1 = __fmaf_rn(__fmaf_rn(-q0, q.s, d), q.r, q0);
-        acc += __float_as_uint(__fadd_rn(q1, kMagicRound)) * (1u << (4 * j));
+      for (int j = 0; j < 8; j += 2) {
+        const float2 d = f2add(make_float2(value(8 * k + j), value(8 * k + j + 1)), nz);
+        const float2 q0 = f2mul(d, r2);
+        const float2 q1 = f2add(__ffma2_rn(__ffma2_rn(q0, ns, d), r2, q0), mg);
+        acc += __float_as_uint(q1.x) * (1u << (4 * j)) + __float_as_uint(q1.y) * (1u << (4 * j + 4));
       }
       nib[k] = acc - kFix;
     }

@@ -61,9 +61,6 @@ struct CodecArgs {
   int64_t payload_bytes;      // decode: caller's payload length
   uint32_t* status;
   const uint32_t* recip;      // [9][2048] reciprocal tables (rc_tables.cuh)
-  uint32_t* model;            // large-alphabet encode: model values, model_blocks * block
-  uint32_t* model_total;      // ... and each block's total after its first halving
-  int64_t model_blocks;       // blocks per batch (0: per-thread model path)
 };
 
 // Fused quantize + range-code kernels (fused_rc.cu): one thread per codec

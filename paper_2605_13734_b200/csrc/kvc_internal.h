@@ -63,8 +63,6 @@ struct Plan {
   int64_t ws_status, ws_streams, ws_heads, ws_packed, ws_slots, ws_sizes, ws_scan;
   int64_t ws_fix;       // fused Hadamard encode: fixup row list (count + rows), or -1
   int64_t ws_delta;     // chunked delta decode: chunk sums / carries / head flags, or -1
-  int64_t ws_model;     // per-symbol model values of the large-alphabet encoder (rc_large.cu)
-  int64_t model_blocks; // blocks per model batch (0 = not used)
   int64_t slot_bytes;   // per-block scratch slot for entropy/rle encode
   int64_t scan_bytes;
   int sm_count;
