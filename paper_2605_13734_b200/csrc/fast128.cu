@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "kernels.h"
@@ -573,7 +574,8 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
 // -- the only way a dequantized or Hadamard-mixed value can be non-finite.
 template <int MODE, int G>
 __device__ __forceinline__ bool dec_core(float* y, const float* sc, const float* zr, int half, int64_t lh,
-                                         const DecArgs& a) {
+                                         const DecArgs& a, const float* aff_rc = nullptr,
+                                         const float* aff_mu = nullptr) {
   static_assert(G >= 32, "fast path groups");
   const Geo& g = a.g;
   bool groups_finite = true;
@@ -637,11 +639,24 @@ __device__ __forceinline__ bool dec_core(float* y, const float* sc, const float*
       Y[16 + i] = f2mul(Y[16 + i], c1);
     }
   } else if (MODE == M_AFFINE) {
-    const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
-    const __half* scl = mu + g.LH * 128;
+    if (aff_rc) {  // the tile's per-channel RN(1/a) and mu from shared memory
+      const float4* rc4 = reinterpret_cast<const float4*>(aff_rc + half * 64);
+      const float4* mu4 = reinterpret_cast<const float4*>(aff_mu + half * 64);
 #pragma unroll
-    for (int i = 0; i < 64; ++i)
-      y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
+      for (int k = 0; k < 16; ++k) {
+        const float4 r = rc4[k], m = mu4[k];
+        y[4 * k] = __fadd_rn(__fmul_rn(y[4 * k], r.x), m.x);
+        y[4 * k + 1] = __fadd_rn(__fmul_rn(y[4 * k + 1], r.y), m.y);
+        y[4 * k + 2] = __fadd_rn(__fmul_rn(y[4 * k + 2], r.z), m.z);
+        y[4 * k + 3] = __fadd_rn(__fmul_rn(y[4 * k + 3], r.w), m.w);
+      }
+    } else {
+      const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
+      const __half* scl = mu + g.LH * 128;
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
+    }
   }
   return groups_finite;
 }
@@ -752,25 +767,35 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(smem_u32(src))
                : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// paged cache view (64 ch, half, head, token row, layer): one box = bt tokens
+// of one head
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int h, int r, int l) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+               "r"(0), "r"(0), "r"(h), "r"(r), "r"(l), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
-template <int W, int G>
+// stage: packed rows, scales, zeros [, affine: the head's fp16 mu and a (256 B each)]
+template <int MODE, int W, int G>
 __host__ __device__ constexpr int dec_stage_bytes() {
-  return 1024 * W + 2 * (64 * (128 / G) * 2);
+  return 1024 * W + 2 * (64 * (128 / G) * 2) + (MODE == M_AFFINE ? 512 : 0);
 }
-template <int W, int G>
+template <int MODE, int W, int G>
 __host__ __device__ constexpr int dec_smem_bytes() {
-  return 2 * kTileBytes + kDecStages * dec_stage_bytes<W, G>() + 1024 + 64;
+  return 2 * kTileBytes + kDecStages * dec_stage_bytes<MODE, W, G>() + 1024 + 64 + (MODE == M_AFFINE ? 4 * 128 * 4 : 0);
 }
 
-template <int MODE, int G, int W>
+template <int MODE, int G, int W, bool PAGED>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__ CUtensorMap omap, const DecArgs a) {
-  constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<W, G>();
+  constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<MODE, W, G>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* obuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* ibuf = obuf + 2 * kTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ibuf + kDecStages * STAGE);
+  // [2][128] RN(1/a), [2][128] mu, double-buffered by tile parity
+  float* aff_tab = reinterpret_cast<float*>(ibuf + kDecStages * STAGE + 64);
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows, nfull = nrows / kRows;
@@ -781,12 +806,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
   constexpr bool had = MODE == M_HADAMARD;
   const int cb0 = had ? 32 * half : 64 * half;
   const int cb1 = had ? 64 + 32 * half : 64 * half + 32;
+  // affine: with whole-head tiles the head's mu / a ride along in the stage
+  const bool tabs = MODE == M_AFFINE && g.T % kRows == 0;
+  const uint8_t* aff_g = a.meta + g.meta_affine_off;
   auto issue = [&](int s, int64_t tile) {
     uint8_t* d = ibuf + s * STAGE;
-    mbar_expect_tx(&full[s], STAGE);
+    mbar_expect_tx(&full[s], (uint32_t)(PK + 2 * SB + (tabs ? 512 : 0)));
     bulk_g2s(d, a.packed + tile * PK, PK, &full[s]);
     bulk_g2s(d + PK, scales + tile * (SB / 2), SB, &full[s]);
     bulk_g2s(d + PK + SB, zeros + tile * (SB / 2), SB, &full[s]);
+    if (tabs) {
+      const int64_t lh = tile * kRows / g.T;
+      bulk_g2s(d + PK + 2 * SB, aff_g + lh * 256, 256, &full[s]);
+      bulk_g2s(d + PK + 2 * SB + 256, aff_g + (g.LH + lh) * 256, 256, &full[s]);
+    }
   };
   if (tid == 0) {
     for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
@@ -830,9 +863,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
       zr[0] = __half2float(zeros[gi0]);
       zr[1] = __half2float(zeros[gi1]);
     }
-    // the output buffer written two tiles ago must have been read out
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    __syncthreads();  // stage s consumed by every thread; obuf[it & 1] free
+    // output: each warp stores its own 16 rows (one TMA box, or one per page
+    // run of the paged cache), so only the input ring needs a CTA barrier;
+    // paged: the warp's page ids are fetched now, long before its store
+    const int warp = tid >> 5, lane = tid & 31;
+    int32_t page_id = 0;
+    const int bt = a.page_tokens < 16 ? (int)a.page_tokens : 16;
+    if (PAGED && lane * bt < 16) {
+      const int64_t t0 = tile * kRows - (tile * kRows / g.T) * g.T + 16 * warp;
+      page_id = a.block_table[(t0 + (int64_t)lane * bt) / a.page_tokens];
+    }
+    float* arc = aff_tab + (it & 1) * 256;
+    float* amu = arc + 128;
+    if (tabs) {  // the tile's per-channel tables from the stage (every tile of the ring is full)
+      const __half* mu = reinterpret_cast<const __half*>(ibuf + s * STAGE + PK + 2 * SB);
+      arc[tid] = __frcp_rn(__half2float(mu[128 + tid]));
+      amu[tid] = __half2float(mu[tid]);
+    }
+    // contiguous output: one tensor store per tile from obuf[it & 1], whose
+    // previous store (two tiles ago) must have been read out
+    if (!PAGED && tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();  // stage s consumed by every thread; affine tables set; obuf[it & 1] free
     if (tid == 0) {
       const int64_t next = tile + (int64_t)kDecStages * gridDim.x;
       if (next < nfull) {
@@ -840,16 +891,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
         issue(s, next);
       }
     }
-    const bool groups_finite = dec_core<MODE, G>(y, sc, zr, half, lh, a);
+    const bool groups_finite =
+        dec_core<MODE, G>(y, sc, zr, half, lh, a, tabs ? arc : nullptr, tabs ? amu : nullptr);
     if (valid) dec_flags<MODE>(y, groups_finite, flags);
-    uint8_t* ob = obuf + (it & 1) * kTileBytes + tid * 128;
+    // paged: this warp's buffer of two tiles ago must have been read out
+    if (PAGED && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    if (PAGED) __syncwarp();
+    uint8_t* wb = obuf + (it & 1) * kTileBytes + warp * 4096;
+    uint8_t* ob = wb + lane * 128;
 #pragma unroll
     for (int k = 0; k < 8; ++k) *reinterpret_cast<uint4*>(ob + (((uint32_t)k ^ sw) << 4)) = pack_bf16x8(y + 8 * k);
     fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) tma_store_2d(&omap, obuf + (it & 1) * kTileBytes, 0, (int)(tile * kThreads));
+    if (!PAGED) {
+      __syncthreads();
+      if (tid == 0) {
+        tma_store_2d(&omap, obuf + (it & 1) * kTileBytes, 0, (int)(tile * kThreads));
+        bulk_commit();
+      }
+    } else {
+      __syncwarp();
+      const int64_t r0 = tile * kRows, lh0 = r0 / g.T, t0 = r0 - lh0 * g.T + 16 * warp;
+      const int l = (int)(lh0 / g.H), h = (int)(lh0 - (int64_t)l * g.H);
+      for (int j = 0; j < 16; j += bt) {
+        const int64_t pg = __shfl_sync(0xffffffffu, page_id, j / bt);
+        const int64_t row = pg * a.page_tokens + (t0 + j) % a.page_tokens;
+        if (lane == 0) tma_store_5d(&omap, wb + j * 256, h, (int)row, l);
+      }
+      if (lane == 0) bulk_commit();
+    }
   }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if ((tid & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
@@ -868,13 +939,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows) {
+bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows, int box_rows = kThreads) {
   auto fn = get_encode_fn();
   if (!fn) return false;
   // the (rows, 128) bf16 tensor viewed as (2*rows, 64): one 128 B half-row per box row
   cuuint64_t dims[2] = {64, (cuuint64_t)(2 * nrows)};
   cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {64, (cuuint32_t)kThreads};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(kv), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -918,23 +989,57 @@ cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count,
 
 // the staged kernel needs a contiguous bf16 output and 16-byte aligned tile
 // bases for the bulk copies (packed rows, scales, zeros)
+// paged cache [pages, page_tokens, H, 128] per layer (layer_stride elements)
+// as a 5-D view (64 channels, half, head, token row, layer); the box is bt
+// tokens of one head, the same 128B-swizzled smem rows as the contiguous map
+bool make_paged_map(CUtensorMap* map, const DecArgs& a, int bt) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  const int64_t row_elems = a.g.H * 128;
+  const int64_t rows = a.layer_stride / row_elems;  // token rows per layer in the pool
+  cuuint64_t dims[5] = {64, 2, (cuuint64_t)a.g.H, (cuuint64_t)rows, (cuuint64_t)a.g.L};
+  cuuint64_t strides[4] = {128, 256, (cuuint64_t)row_elems * 2, (cuuint64_t)a.layer_stride * 2};
+  cuuint32_t box[5] = {64, 2, 1, (cuuint32_t)bt, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, a.out, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <typename Tout, int W>
 bool dec_staged_ok(const DecArgs& a) {
-  if (sizeof(Tout) != 2 || W == 0 || a.paged) return false;
+  if (sizeof(Tout) != 2 || W == 0) return false;
   const int64_t nrows = a.g.LH * a.g.T;
   if (2 * nrows >= (1ll << 31)) return false;
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  return al(a.packed) && al(a.meta) && al(a.out) && (a.g.ngroups % 8) == 0;
+  if (!(al(a.packed) && al(a.meta) && al(a.out) && (a.g.ngroups % 8) == 0)) return false;
+  if (a.paged) {
+    // whole 64-token tiles of one head, page runs of >= 4 tokens (1 KB-aligned
+    // smem sub-boxes), a per-layer pool extent
+    const int64_t pt = a.page_tokens, row_elems = a.g.H * 128;
+    if (a.g.T % kRows != 0 || pt < 4 || (pt < 16 ? 16 % pt : pt % 16) != 0) return false;
+    if (a.layer_stride <= 0 || a.layer_stride % row_elems != 0 || (a.layer_stride * 2) % 16 != 0) return false;
+    if (a.layer_stride / row_elems >= (1ll << 31)) return false;
+  }
+  return true;
 }
 
 template <int MODE, typename Tout, int G, int W>
 cudaError_t launch_dec_gw(const DecArgs& a, int sm_count, cudaStream_t s) {
   if constexpr (sizeof(Tout) == 2 && W != 0) {
     CUtensorMap omap;
-    if (dec_staged_ok<Tout, W>(a) && make_input_map(&omap, a.out, a.g.LH * a.g.T)) {
-      auto k = k_dec128r<MODE, G, W>;
-      constexpr int smem = dec_smem_bytes<W, G>();
-      set_max_dyn_smem<k_dec128r<MODE, G, W>>(smem);
+    const bool mapped = dec_staged_ok<Tout, W>(a) &&
+                        (a.paged ? make_paged_map(&omap, a, (int)std::min<int64_t>(a.page_tokens, 16))
+                                 : make_input_map(&omap, a.out, a.g.LH * a.g.T));
+    if (mapped) {
+      auto k = a.paged ? k_dec128r<MODE, G, W, true> : k_dec128r<MODE, G, W, false>;
+      constexpr int smem = dec_smem_bytes<MODE, W, G>();
+      if (a.paged) {
+        set_max_dyn_smem<k_dec128r<MODE, G, W, true>>(smem);
+      } else {
+        set_max_dyn_smem<k_dec128r<MODE, G, W, false>>(smem);
+      }
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
       if (per_sm < 1) per_sm = 1;
