@@ -142,7 +142,7 @@ def reference_arm(args, wl, rank):
         "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": procs, "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------
@@ -506,10 +506,24 @@ def main():
             "rank_compressed_bytes": all_sizes,
             "wall_s": round(wall, 3),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
 
+# stdout carries exactly the one JSON line: every other write to fd 1 (NCCL's
+# version banner, library chatter from C code) is sent to stderr
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 if __name__ == "__main__":
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     main()
