@@ -146,6 +146,53 @@ def reference_arm(args, wl, rank):
 
 
 # ----------------------------------------------------------------------------
+# ncu evidence for the dominant kernel (committed captures under profiles/)
+# ----------------------------------------------------------------------------
+_NCU_KERNELS = {
+    "fused_encode": ("k_fused_tok_encode", "k_fused_chan_encode"),
+    "fused_decode": ("k_fused_tok_decode", "k_fused_chan_decode"),
+    "encode_fast128": ("k_enc128",), "decode_fast128": ("k_dec128",),
+    "rc_encode": ("k_rc_large_encode", "k_rc_small_encode"), "rc_decode": ("k_rc_large_decode", "k_rc_small_decode"),
+    "gather": ("k_gather",),
+}
+
+
+def _ncu_evidence(workload: str, scope: str):
+    """Per-launch DRAM bytes, warp instructions and issue-active % of the
+    kernels behind `scope`, averaged over the launches in the newest
+    profiles/r*/ncu_full_<workload>_raw.csv (tools/prof_one.sh), or None."""
+    import csv
+    import glob
+
+    names = _NCU_KERNELS.get(scope)
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_full_{workload}_raw.csv")))
+    if not names or not paths:
+        return None
+    unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1.0, "%": 1.0}
+    try:
+        rows = list(csv.reader(open(paths[-1])))
+        h, u = rows[0], rows[1]
+        col = {n: h.index(n) for n in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                        "smsp__inst_executed.sum",
+                                        "smsp__issue_active.avg.pct_of_peak_sustained_active")}
+        acc, n = [0.0, 0.0, 0.0], 0
+        for r in rows[2:]:
+            if not any(k in r[col["Kernel Name"]] for k in names):
+                continue
+            v = lambda key: float(r[col[key]].replace(",", "")) * unit.get(u[col[key]], 1.0)  # noqa: E731
+            acc[0] += v("dram__bytes_read.sum") + v("dram__bytes_write.sum")
+            acc[1] += v("smsp__inst_executed.sum")
+            acc[2] += v("smsp__issue_active.avg.pct_of_peak_sustained_active")
+            n += 1
+        if n == 0:
+            return None
+        return {"dram_bytes": acc[0] / n, "inst": acc[1] / n, "issue_pct": acc[2] / n,
+                "source": os.path.relpath(paths[-1], ROOT)}
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
 # clocks during the timed region
 # ----------------------------------------------------------------------------
 
@@ -415,10 +462,26 @@ def main():
     if bytes_list:
         per_launch_bytes = sum(bytes_list) / len(bytes_list)
         achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        ev = _ncu_evidence(args.workload, dom_name)
         roofline = {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 2), "peak": hbm_peak,
-                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                    "traffic": round(ev["dram_bytes"]) if ev else None,
                     "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
                     "share_of_step": round(dom_ms / prof_steps / step_ms, 3)}
+        if ev:
+            # the serial range coders are instruction-bound: warp-instructions
+            # per launch (same capture) over this run's launch time, against
+            # 4 issue slots per SM per cycle at the measured SM clock
+            roofline["traffic_source"] = ev["source"]
+            roofline["issue"] = {"warp_inst_per_launch": round(ev["inst"]),
+                                 "achieved_tinst_s": round(ev["inst"] / (per_launch_ms * 1e-3) / 1e12, 3),
+                                 "ncu_issue_active_pct": round(ev["issue_pct"], 1)}
+            mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz")
+            if mhz:
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                peak_i = sms * 4 * mhz * 1e6
+                roofline["issue"]["peak_tinst_s"] = round(peak_i / 1e12, 3)
+                roofline["issue"]["frac"] = round(ev["inst"] / (per_launch_ms * 1e-3) / peak_i, 4)
     step_alg = 2 * sum(2 * E + t["blob"].compressed_nbytes for t in tensors)
     kernels = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] / prof_steps} for k, v in prof.items()}
 
