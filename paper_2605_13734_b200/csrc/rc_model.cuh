@@ -57,6 +57,43 @@ struct SModel {
 #pragma unroll
     for (int k = 1; k < A; ++k) C[k] += (s < (uint32_t)k) ? 32u : 0u;
   }
+  // Decoder search for A = 8, 16 without the division: binary search over
+  // the cumulative counts, s = largest with x >= unit * C[s] (<=> floor(x /
+  // unit) >= C[s]; the reference's clamp to total - 1 never changes s since
+  // C[A-1] <= total - 1).  Level `bit` compares against C[s + bit], chosen
+  // among the A / (2 bit) candidates by a select tree on the bits decided so
+  // far; plo / phi are the last accepted / rejected unit * C (unit * tot if
+  // none rejected).
+  __device__ __forceinline__ uint32_t bsearch(uint32_t x, uint32_t unit, uint32_t tot, uint32_t& plo,
+                                              uint32_t& phi) const {
+    uint32_t s = 0;
+    plo = 0;
+    phi = unit * tot;
+#pragma unroll
+    for (int L = W - 1; L >= 0; --L) {
+      const uint32_t bit = 1u << L;
+      constexpr int kMax = A / 2;
+      uint32_t cand[kMax];
+      const int n = A / (2 * (int)bit);  // candidates C[(2i + 1) bit], i = s / (2 bit)
+#pragma unroll
+      for (int i = 0; i < kMax; ++i)
+        if (i < n) cand[i] = C[(2 * i + 1) * bit];
+      // select tree: fold pairs by the decided bits, lowest decided bit first
+#pragma unroll
+      for (int lev = 0; (1 << lev) < n; ++lev) {
+        const bool hi = (s >> (L + 1 + lev)) & 1u;
+#pragma unroll
+        for (int i = 0; i < kMax / 2; ++i)
+          if (2 * i + 1 < (n >> lev)) cand[i] = hi ? cand[2 * i + 1] : cand[2 * i];
+      }
+      const uint32_t v = unit * cand[0];
+      const bool ok = x >= v;
+      s += ok ? bit : 0u;
+      plo = ok ? v : plo;
+      phi = ok ? phi : v;
+    }
+    return s;
+  }
   __device__ __forceinline__ uint32_t find_t(uint32_t x, uint32_t unit, uint32_t tot, uint32_t& plo,
                                              uint32_t& phi) const {
     if constexpr (A <= 4) {
@@ -74,19 +111,7 @@ struct SModel {
       }
       return s;
     } else {
-      uint32_t target = x / unit;
-      target = target < tot - 1 ? target : tot - 1;
-      uint32_t s = 0, lo = 0, hi = C[1];
-#pragma unroll
-      for (int k = 1; k < A; ++k) {
-        const bool ge = target >= C[k];
-        s += ge ? 1u : 0u;
-        lo = ge ? C[k] : lo;
-        hi = ge ? (k + 1 < A ? C[k + 1] : tot) : hi;
-      }
-      plo = unit * lo;
-      phi = unit * hi;
-      return s;
+      return bsearch(x, unit, tot, plo, phi);
     }
   }
   // Encoder step for the fused kernels: (lo, hi) = (C[s], C[s+1]) and then
@@ -171,19 +196,7 @@ struct SModel {
       }
       return s;
     } else {
-      uint32_t target = x / unit;
-      target = target < total - 1 ? target : total - 1;
-      uint32_t s = 0, lo = 0, hi = C[1];
-#pragma unroll
-      for (int k = 1; k < A; ++k) {
-        const bool ge = target >= C[k];
-        s += ge ? 1u : 0u;
-        lo = ge ? C[k] : lo;
-        hi = ge ? (k + 1 < A ? C[k + 1] : total) : hi;
-      }
-      plo = unit * lo;
-      phi = unit * hi;
-      return s;
+      return bsearch(x, unit, total, plo, phi);
     }
   }
 };

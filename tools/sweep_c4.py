@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--limit", type=int, default=0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--match", default="", help="only ids containing all of these comma-separated substrings")
     args = ap.parse_args()
 
     import torch
@@ -72,6 +73,8 @@ def main():
         kvs.append(KVTensor(kv, imp))
     timer = CudaEventTimer(repeats=3, warmup=1)
     ids = candidates()
+    if args.match:
+        ids = [i for i in ids if all(m in i for m in args.match.split(","))]
     if args.limit:
         ids = ids[: args.limit]
     out = open(args.out, "w") if args.out else None
