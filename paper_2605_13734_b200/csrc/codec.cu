@@ -58,20 +58,41 @@ __device__ void rle_encode_block(const uint8_t* src, int n, uint8_t* slot, int64
   (void)status;
   VecReader rd;
   rd.init(src);
+  // output bytes collect in a little-endian word and leave as 32-bit stores
+  // (the slot is 16-byte aligned); a literal chunk's control byte is patched
+  // in the word if it is still open, else by one byte store
+  uint32_t* sw = reinterpret_cast<uint32_t*>(slot);
+  uint32_t acc = 0;
   int pos = 0;         // output position
   int lit_ctrl = -1;   // position of the open literal chunk's control byte
   int lit_len = 0;
+  auto put = [&](uint32_t b) {
+    acc |= b << (8 * (pos & 3));
+    if ((pos & 3) == 3) {
+      sw[pos >> 2] = acc;
+      acc = 0;
+    }
+    ++pos;
+  };
+  auto patch = [&](int at, uint32_t b) {
+    if ((at >> 2) == (pos >> 2)) {
+      acc |= b << (8 * (at & 3));
+    } else {
+      slot[at] = (uint8_t)b;
+    }
+  };
   auto lit_byte = [&](uint32_t b) {
     if (lit_ctrl < 0 || lit_len == 128) {
-      if (lit_ctrl >= 0) slot[lit_ctrl] = (uint8_t)(lit_len - 1);
-      lit_ctrl = pos++;
+      if (lit_ctrl >= 0) patch(lit_ctrl, (uint32_t)(lit_len - 1));
+      lit_ctrl = pos;
+      put(0u);  // placeholder for the control byte
       lit_len = 0;
     }
-    slot[pos++] = (uint8_t)b;
+    put(b);
     ++lit_len;
   };
   auto lit_close = [&]() {
-    if (lit_ctrl >= 0) slot[lit_ctrl] = (uint8_t)(lit_len - 1);
+    if (lit_ctrl >= 0) patch(lit_ctrl, (uint32_t)(lit_len - 1));
     lit_ctrl = -1;
     lit_len = 0;
   };
@@ -94,8 +115,8 @@ __device__ void rle_encode_block(const uint8_t* src, int n, uint8_t* slot, int64
       int r = run;
       while (r >= 3) {
         const int ch = r < 130 ? r : 130;
-        slot[pos++] = (uint8_t)(128 + ch - 3);
-        slot[pos++] = (uint8_t)v;
+        put((uint32_t)(128 + ch - 3));
+        put(v);
         r -= ch;
       }
       for (int k = 0; k < r; ++k) lit_byte(v);  // leftover < 3 starts a literal
@@ -106,6 +127,7 @@ __device__ void rle_encode_block(const uint8_t* src, int n, uint8_t* slot, int64
     if (more) v = nb;
   }
   lit_close();
+  if (pos & 3) sw[pos >> 2] = acc;  // the partial last word (bytes past pos are slack)
   *size_out = (uint64_t)pos;
 }
 
