@@ -235,14 +235,6 @@ __device__ __forceinline__ void minmax32_bf16(const uint32_t* w, float& mn, floa
   mx = __uint_as_float(hi << 16);
 }
 
-// true iff any of the 64 bf16 values packed in w[0..31] is NaN or +-inf
-__device__ __forceinline__ bool nonfinite64_bf16(const uint32_t* w) {
-  uint32_t m = w[0] & 0x7FFF7FFFu;
-#pragma unroll
-  for (int k = 1; k < 32; ++k) m = bmax2(m, w[k] & 0x7FFF7FFFu);
-  return ((m & 0x7F80u) == 0x7F80u) | ((m & 0x7F800000u) == 0x7F800000u);
-}
-
 // Quantize the thread's 64 values (two chunks of 32 at channel bases cb0,
 // cb1) given each chunk's min/max; G in {32, 64, 128}: a 64-group is both
 // chunks (natural layout) or chunk c of both threads of the row (hadamard
