@@ -136,19 +136,26 @@ struct LModel {
   // node address is known up front and the loads issue together
   template <bool UPD>
   __device__ __forceinline__ void lookup_upd(uint32_t s, uint32_t& cum, uint32_t& fr) {
+    // all loads first, then the stores: the path's nodes are distinct, and a
+    // store between two loads would serialize the loads behind its data
     const uint32_t q0 = col();
-    uint32_t acc = 0, hi = total;
+    uint32_t na[W], t[W];
 #pragma unroll
     for (int k = W - 1; k >= 0; --k) {
       const uint32_t bit = 1u << k;
       const uint32_t pre = s & ~(2 * bit - 1);  // pos at this level
-      const uint32_t na = q0 + pre * (2 * kLThreads) + off(bit);
-      const uint32_t t = lds16(na);
+      na[k] = q0 + pre * (2 * kLThreads) + off(bit);
+      t[k] = lds16(na[k]);
+    }
+    uint32_t acc = 0, hi = total;
+#pragma unroll
+    for (int k = W - 1; k >= 0; --k) {
+      const uint32_t bit = 1u << k;
       if (s & bit) {
-        acc += t;
+        acc += t[k];
       } else {
-        hi = acc + t;  // the last rejected node ends at s + 1
-        if (UPD) sts16(na, t + 32u);
+        hi = acc + t[k];  // the last rejected node ends at s + 1
+        if (UPD) sts16(na[k], t[k] + 32u);
       }
     }
     cum = acc;
