@@ -174,3 +174,29 @@ def test_paged_delta_long_sequence_chunked():
         codec.check(decoding=True)
         pv = pages.view(L, npages, P, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
         assert torch.equal(pv, flat), sid
+
+
+@pytest.mark.parametrize("T,P", [(200, 8), (240, 16), (256, 32)])
+def test_paged_decode_ragged_tokens(T, P):
+    """Token counts that do not tile 64-row (T = 200, 240: the direct paged
+    kernel) and a page run of 32 (the staged kernel) give the contiguous
+    decode's values in the paged cache."""
+    from paper_2605_13734_b200 import KVCodec
+
+    L, H, C = 2, 3, 128
+    v, _ = oracle.generate_kv(L, H, T, C, seed=T + P)
+    kv = torch.from_numpy(v).to(torch.bfloat16).cuda()
+    for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=affine;q=uniform,b=8,g=32;c=entropy",
+                "t=identity;q=uniform,b=2,g=64;c=none"):
+        codec = KVCodec(sid, (L, H, T, C))
+        blob = codec.encode(kv)
+        flat = codec.decode(blob)
+        npages = -(-T // P) + 2
+        table = torch.randperm(npages, device="cuda")[: -(-T // P)].to(torch.int32)
+        pages = torch.zeros(L * npages * P * H * C, dtype=torch.bfloat16, device="cuda")
+        codec.decode_paged(blob, pages, table, P, npages * P * H * C)
+        codec.check(decoding=True)
+        pv = pages.view(L, npages * P, H, C)
+        rows = (table.long()[:, None] * P + torch.arange(P, device="cuda")[None, :]).reshape(-1)[:T]
+        got = pv[:, rows].permute(0, 2, 1, 3)
+        assert torch.equal(got, flat), sid
