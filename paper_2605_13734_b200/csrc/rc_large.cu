@@ -301,6 +301,25 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
     // positions before the halving: total 2^W + 32 i, reciprocal loaded one
     // symbol ahead, updates folded into the descent, one word out per 32 bits
     const int n1 = min(n, H - 1);
+    if constexpr (W == 8) {
+      // four symbols per word: unrolled, one store per four
+      const int n4 = n1 & ~3;
+      for (; i < n4; i += 4) {
+        uint32_t wd = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const unsigned mask = __activemask();
+          const uint32_t unit = div_recip(d.range, (uint32_t)A + 32u * (uint32_t)(i + j), magic[i + j]);
+          uint32_t plo, phi;
+          const uint32_t s = m.template find_scaled_upd<true>(d.offset(), unit, plo, phi);
+          d.advance_warp(plo, phi, mask);
+          m.total += 32u;
+          wd |= s << (8 * j);  // little-endian byte j = symbol i + j
+        }
+        *reinterpret_cast<uint32_t*>(dst + nout) = wd;
+        nout += 4;
+      }
+    }
     for (; i < n1; ++i) {
       const unsigned mask = __activemask();
       const uint32_t unit = div_recip(d.range, (uint32_t)A + 32u * (uint32_t)i, magic[i]);
