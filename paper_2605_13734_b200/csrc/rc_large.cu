@@ -210,6 +210,25 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
     uint64_t win = 0;
     int nbits = 0;
     const int n1 = min(n, H - 1);
+    if constexpr (W == 8) {
+      // four symbols per loaded word (byte j = symbol 4q + j), unrolled; the
+      // next word is loaded one step ahead
+      const int n4 = n1 & ~3;
+      for (; i < n4; i += 4) {
+        const uint32_t cur = nxt;
+        nxt = __ldg(wp + min(++wi, nw - 1));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const unsigned mask = __activemask();
+          const uint32_t s = (cur >> (8 * j)) & 0xFFu;
+          uint32_t cum, fr;
+          m.template lookup_upd<true>(s, cum, fr);
+          e.encode_warp(div_recip(e.range, (uint32_t)A + 32u * (uint32_t)(i + j), magic[i + j]), cum, fr, mask);
+          m.total += 32u;
+        }
+      }
+      // the word-window loop below continues at word wi (nbits == 0)
+    }
     for (; i < n1; ++i) {
       const unsigned mask = __activemask();
       if (nbits < W) {
