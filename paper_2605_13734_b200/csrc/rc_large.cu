@@ -90,13 +90,16 @@ struct LModel {
   // 32-bit shared-window address of the thread's column (no generic pointer
   // arithmetic in the descents)
   __device__ __forceinline__ uint32_t col() const { return (uint32_t)__cvta_generic_to_shared(tree); }
+  // 16-bit nodes moved through 32-bit registers (zero-extended on load,
+  // truncated on store): selects between loaded nodes stay plain SELs instead
+  // of 16-bit merges plus a mask
   __device__ __forceinline__ static uint32_t lds16(uint32_t addr) {
-    unsigned short v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
   }
   __device__ __forceinline__ static void sts16(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "r"(v));
   }
   // decoder: s = largest with unit * prefix(s) <= x; plo / phi as find_scaled
   template <bool UPD>
@@ -215,11 +218,11 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_encode(CodecArgs a) {
       // next word is loaded one step ahead
       const int n4 = n1 & ~3;
       for (; i < n4; i += 4) {
+        const unsigned mask = __activemask();  // the same lanes code all four
         const uint32_t cur = nxt;
         nxt = __ldg(wp + min(++wi, nw - 1));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const unsigned mask = __activemask();
           const uint32_t s = (cur >> (8 * j)) & 0xFFu;
           uint32_t cum, fr;
           m.template lookup_upd<true>(s, cum, fr);
@@ -324,10 +327,10 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
       // four symbols per word: unrolled, one store per four
       const int n4 = n1 & ~3;
       for (; i < n4; i += 4) {
+        const unsigned mask = __activemask();  // the same lanes decode all four
         uint32_t wd = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const unsigned mask = __activemask();
           const uint32_t unit = div_recip(d.range, (uint32_t)A + 32u * (uint32_t)(i + j), magic[i + j]);
           uint32_t plo, phi;
           const uint32_t s = m.template find_scaled_upd<true>(d.offset(), unit, plo, phi);
