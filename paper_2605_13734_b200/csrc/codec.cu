@@ -264,10 +264,23 @@ __global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
     uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
     const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
-    for (uint32_t w = lane; w < words; w += 32) {
-      const uint32_t lo = s32[w];
-      const uint32_t v = sh ? __funnelshift_r(lo, s32[w + 1], sh) : lo;
-      d32[w] = v;
+    // U words per lane per round, all loads issued before any store (slots
+    // and payload never overlap, but the compiler cannot know that and would
+    // otherwise serialize each load behind the previous store)
+    constexpr uint32_t U = 4;
+    for (uint32_t w0 = lane; w0 < words; w0 += 32 * U) {
+      uint32_t lo[U], hi[U];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t w = w0 + 32 * u;
+        lo[u] = w < words ? __ldg(s32 + w) : 0u;
+        hi[u] = (w < words && sh) ? __ldg(s32 + w + 1) : 0u;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t w = w0 + 32 * u;
+        if (w < words) d32[w] = sh ? __funnelshift_r(lo[u], hi[u], sh) : lo[u];
+      }
     }
     o0 = n0;
     o1 = n1;
