@@ -748,7 +748,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
 // memory in the 128B-swizzled TMA layout (conflict-free 16 B stores) and
 // leaves as one tensor store (double-buffered, bulk_group).  The partial last
 // tile reads its inputs directly; the tensor store clips rows past the end.
-constexpr int kDecStages = 3;
+// input ring depth: 3 stages, 2 for 8-bit rows (their 8 KB stages would
+// otherwise hold the kernel at 3 CTAs/SM; with 2 it fits 4)
+template <int W>
+__host__ __device__ constexpr int dec_stages() {
+  return W >= 8 ? 2 : 3;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -776,18 +781,19 @@ __host__ __device__ constexpr int dec_stage_bytes() {
 }
 template <int MODE, int W, int G>
 __host__ __device__ constexpr int dec_smem_bytes() {
-  return 2 * kTileBytes + kDecStages * dec_stage_bytes<MODE, W, G>() + 1024 + 64 + (MODE == M_AFFINE ? 4 * 128 * 4 : 0);
+  return 2 * kTileBytes + dec_stages<W>() * dec_stage_bytes<MODE, W, G>() + 1024 + 64 + (MODE == M_AFFINE ? 4 * 128 * 4 : 0);
 }
 
 template <int MODE, int G, int W, bool PAGED>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__ CUtensorMap omap, const DecArgs a) {
+  constexpr int NS = dec_stages<W>();
   constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<MODE, W, G>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* obuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* ibuf = obuf + 2 * kTileBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ibuf + kDecStages * STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ibuf + NS * STAGE);
   // [2][128] RN(1/a), [2][128] mu, double-buffered by tile parity
-  float* aff_tab = reinterpret_cast<float*>(ibuf + kDecStages * STAGE + 64);
+  float* aff_tab = reinterpret_cast<float*>(ibuf + NS * STAGE + 64);
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows, nfull = nrows / kRows;
@@ -814,12 +820,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
     }
   };
   if (tid == 0) {
-    for (int s = 0; s < kDecStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < kDecStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < nfull) issue(s, tile);
     }
@@ -827,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
   uint32_t flags = 0;
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int s = it % kDecStages;
+    const int s = it % NS;
     const int64_t row0 = tile * kRows + lr;
     const bool valid = row0 < nrows;
     const int64_t row = valid ? row0 : nrows - 1;
@@ -835,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
     __align__(8) float y[64];
     float sc[2], zr[2];
     if (tile < nfull) {
-      mbar_wait(&full[s], (uint32_t)((it / kDecStages) & 1));
+      mbar_wait(&full[s], (uint32_t)((it / NS) & 1));
       const uint8_t* st = ibuf + s * STAGE;
       unpack32<W, true>(st + lr * 16 * W + cb0 * W / 8, y);
       unpack32<W, true>(st + lr * 16 * W + cb1 * W / 8, y + 32);
@@ -877,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
     if (!PAGED && tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     __syncthreads();  // stage s consumed by every thread; affine tables set; obuf[it & 1] free
     if (tid == 0) {
-      const int64_t next = tile + (int64_t)kDecStages * gridDim.x;
+      const int64_t next = tile + (int64_t)NS * gridDim.x;
       if (next < nfull) {
         fence_proxy_async();
         issue(s, next);
