@@ -5,19 +5,28 @@ One step = the reference's compress() round trip (compress.py:111-140) for
 every KV tensor of the workload: encode (transform -> quantize -> lossless
 codec) then decode (codec -> dequantize -> inverse transform) back to bf16,
 inputs and outputs resident in HBM.  `value` is bf16-in GB/s of that round
-trip, V / (t_enc + t_dec) — the reference's s_p (compress.py:32-40) — summed
-over ranks; compress and decompress GB/s are reported separately.
+trip, V / (t_enc + t_dec) -- the reference's s_p (compress.py:32-40) --
+summed over ranks; compress and decompress GB/s are reported separately.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1|c3|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c5]
+                    [--impl ours|reference] [--no-extras]
 
-Workloads (BASELINE.json configs; c2 = configs[1] is the default headline):
-  c1  Llama-3.1-8B 4K   (32,8,4096,128)   K,V: t=hadamard;q=uniform,b=4,g=32;c=none
+Workloads (BASELINE.json configs; c3 = the north-star scaling config, the
+largest single-GPU config, is the headline):
+  c3  Llama-3.1-70B 128K (80,8,128000,128) K,V: t=hadamard;q=uniform,b=4,g=32;c=none,
+                                           layers sharded over ranks (strong scaling)
+  c1  Llama-3.1-8B 4K   (32,8,4096,128)   K,V: the same reference default profile
   c2  Llama-3.1-8B 32K  (32,8,32768,128)  K: t=identity;q=uchan,b=2,g=32;c=entropy (KIVI per-channel)
                                            V: t=identity;q=uniform,b=2,g=32;c=entropy (per-token)
-  c3  Llama-3.1-70B 128K (80,8,128000,128) K,V: C1 profile, layers sharded over ranks (strong scaling)
   c5  Qwen3-8B 16K      (36,8,16384,128)  K,V: t=affine;q=uniform,b=8,g=32;c=entropy, decoded into paged KV
-Multi-GPU: torchrun, one process per GPU; no collective on the data path —
-only the per-rank compressed sizes are all-gathered (offsets for the wire).
+At N=1 the default run also measures c1, c2 and c5 and nests them under
+"extra" (same fields, fewer steps).  Multi-GPU: torchrun, one process per
+GPU; no collective on the data path -- only the per-rank compressed sizes
+are all-gathered (offsets for the wire).
+
+--impl reference: the reference pipeline's CPU implementation -- the oracle
+port (oracle/, the reference is Python and cannot travel to the GPU box) --
+on all host cores, same metric / config / unit as this arm.
 """
 
 from __future__ import annotations
@@ -35,21 +44,26 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "KV compress+decompress round-trip GB/s (bf16-in)"
 C1_PROFILE = "t=hadamard;q=uniform,b=4,g=32;c=none"
 WORKLOADS = {
+    "c3": dict(name="Llama-3.1-70B KV 128K tokens, reference default profile, layer-sharded", shape=(80, 8, 128000, 128),
+               tensors=[("K", C1_PROFILE), ("V", C1_PROFILE)], shard=True, paged=False),
     "c1": dict(name="Llama-3.1-8B KV 4K tokens, reference default profile", shape=(32, 8, 4096, 128),
                tensors=[("K", C1_PROFILE), ("V", C1_PROFILE)], shard=False, paged=False),
     "c2": dict(name="Llama-3.1-8B KV 32K tokens, KIVI 2-bit per-channel K / per-token V + entropy",
                shape=(32, 8, 32768, 128),
                tensors=[("K", "t=identity;q=uchan,b=2,g=32;c=entropy"), ("V", "t=identity;q=uniform,b=2,g=32;c=entropy")],
                shard=False, paged=False),
-    "c3": dict(name="Llama-3.1-70B KV 128K tokens, layer-sharded", shape=(80, 8, 128000, 128),
-               tensors=[("K", C1_PROFILE), ("V", C1_PROFILE)], shard=True, paged=False),
     "c5": dict(name="Qwen3-8B GQA KV 16K tokens, affine + 8-bit + entropy, paged decode", shape=(36, 8, 16384, 128),
                tensors=[("K", "t=affine;q=uniform,b=8,g=32;c=entropy"), ("V", "t=affine;q=uniform,b=8,g=32;c=entropy")],
                shard=False, paged=True),
 }
+EXTRAS = ("c1", "c2", "c5")
+EXTRA_STEPS = 5
 BLOCK = 2048
+PAGE_TOKENS = 16
+CPU_TOKENS = 8192  # tokens per head slab in the CPU samples
 
 
 def _args():
@@ -57,17 +71,26 @@ def _args():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    p.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-extras", action="store_true", help="headline workload only")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--block", type=int, default=None, help="codec block symbols (default 2048)")
-    p.add_argument("--streams", type=int, default=1, help="1: one CUDA stream per KV tensor (default); 0: serial")
+    p.add_argument("--serial", action="store_true", help="K and V on one stream (default: one stream each)")
     args = p.parse_args()
     global BLOCK
     if args.block:
         BLOCK = args.block
     return args
+
+
+def config_of(workload: str, world: int) -> dict:
+    """The `config` object, identical in both arms."""
+    wl = WORKLOADS[workload]
+    return {"workload": workload, "name": wl["name"], "shape": list(wl["shape"]), "tensors": dict(wl["tensors"]),
+            "block_symbols": BLOCK, "paged": wl["paged"], "l2": "inputs larger than L2 (no flush needed)",
+            "parallelism": (f"layer-sharded x{world} (strong)" if wl["shard"] else f"dp{world} independent caches (weak)")}
 
 
 def _shard_shape(wl, rank, world):
@@ -80,67 +103,104 @@ def _shard_shape(wl, rank, world):
 
 
 # ----------------------------------------------------------------------------
-# CPU side: the oracle (CPU restatement of the reference) on host cores
+# CPU side: the reference pipeline's CPU implementation (the oracle port) on
+# the host cores.  Inputs are generated in the parent BEFORE the worker pool
+# forks; only encode + decode run inside the timed region.
 # ----------------------------------------------------------------------------
+_CPU_SLABS: list = []
 
-def _oracle_slab(job):
-    """Round trip of one (1 layer, 1 head) slab through the oracle; returns
-    (bf16 bytes, seconds).  Runs in a worker process."""
-    import numpy as np
 
+def _cpu_slab(i):
+    """Round trip of pre-generated head slab i through the oracle; runs in a
+    pool worker; returns (bf16 bytes, seconds)."""
     import oracle
 
-    sid, tokens, channels, seed = job
-    v, imp = oracle.generate_kv(1, 1, tokens, channels, seed=seed)
-    u = v.view(np.uint32).astype(np.uint64)
-    v = ((((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32)).view(np.float32)  # bf16-exact
+    sid, v, imp = _CPU_SLABS[i]
     t0 = time.perf_counter()
     ob = oracle.encode_blob(v, imp, sid, block=BLOCK)
     oracle.decode_blob(ob["payload"], ob["metadata"], ob["offsets"], sid, v.shape, block=BLOCK)
     return v.size * 2, time.perf_counter() - t0
 
 
-def cpu_roundtrip(wl, n_slabs, procs, seed0=1000):
-    """bf16-in GB/s of the oracle round trip over `n_slabs` head slabs."""
-    import multiprocessing as mp
-
-    _, H, T, C = wl["shape"]
-    tok = min(T, 8192)
-    jobs = [(wl["tensors"][i % len(wl["tensors"])][1], tok, C, seed0 + i) for i in range(n_slabs)]
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
-        res = pool.map(_oracle_slab, jobs, chunksize=1)
-    wall = time.perf_counter() - t0
-    nbytes = sum(r[0] for r in res)
-    return nbytes / wall / 1e9, nbytes, wall, tok
+def _cpu_ping(_):
+    return os.getpid()
 
 
-def reference_arm(args, wl, rank):
+class CpuBaseline:
+    """The oracle round trip of `slabs_per_step` head slabs per step, one
+    slab per worker process (all host cores); value = bytes / wall seconds
+    of the codec work only (pool started and inputs generated beforehand)."""
+
+    def __init__(self, workload: str, slabs_per_step: int, steps: int, seed0: int = 1000):
+        import multiprocessing as mp
+
+        import numpy as np
+
+        import oracle
+
+        wl = WORKLOADS[workload]
+        _, _, T, C = wl["shape"]
+        self.tok = min(T, CPU_TOKENS)
+        self.procs = len(os.sched_getaffinity(0))
+        self.per_step = slabs_per_step
+        self.steps = steps
+        _CPU_SLABS.clear()
+        for i in range(slabs_per_step * steps):
+            sid = wl["tensors"][i % len(wl["tensors"])][1]
+            v, imp = oracle.generate_kv(1, 1, self.tok, C, seed=seed0 + i)
+            u = v.view(np.uint32).astype(np.uint64)
+            v = ((((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32)).view(np.float32)  # bf16-exact
+            _CPU_SLABS.append((sid, v, imp))
+        self.pool = mp.get_context("fork").Pool(self.procs)
+        self.pool.map(_cpu_ping, range(self.procs), chunksize=1)  # workers up before any timing
+
+    def run_step(self, k: int) -> tuple[int, float]:
+        idx = list(range(k * self.per_step, (k + 1) * self.per_step))
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_slab, idx, chunksize=1)
+        return sum(r[0] for r in res), time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+        _CPU_SLABS.clear()
+
+    def sample(self, C: int) -> str:
+        return (f"{self.per_step} head slabs per step x {self.tok} tokens x {C} ch of this workload's strategies "
+                f"(bf16-exact reference-generator data), oracle encode+decode on {self.procs} worker processes")
+
+
+def cpu_measure(workload: str, steps: int, warmup: int) -> dict:
+    """cpu_baseline object for `workload` (the same figure the reference arm reports)."""
+    procs = len(os.sched_getaffinity(0))
+    cb = CpuBaseline(workload, procs, warmup + steps)
+    try:
+        for k in range(warmup):
+            cb.run_step(k)
+        nb = wall = 0.0
+        for k in range(warmup, warmup + steps):
+            b, w = cb.run_step(k)
+            nb += b
+            wall += w
+    finally:
+        cb.close()
+    return {"value": round(nb / wall / 1e9, 6), "unit": "GB/s", "cores": procs, "kind": "port",
+            "sample": cb.sample(WORKLOADS[workload]["shape"][3]), "ms_per_step": round(1e3 * wall / steps, 3)}
+
+
+def reference_arm(args, rank, world):
     """--impl reference: the oracle port of the reference pipeline on all host cores."""
     if rank != 0:
         return
-    procs = len(os.sched_getaffinity(0))
-    for _ in range(max(args.warmup, 0) and 1):
-        cpu_roundtrip(wl, procs, procs, seed0=1)
-    vals, total_bytes, total_wall = [], 0, 0.0
-    tok = None
-    for k in range(args.steps):
-        gbs, nb, wall, tok = cpu_roundtrip(wl, procs, procs, seed0=100 + k * procs)
-        vals.append(gbs)
-        total_bytes += nb
-        total_wall += wall
-    value = total_bytes / total_wall / 1e9
-    sample = f"{procs} head slabs x {tok} tokens x {wl['shape'][3]} ch per step ({procs} processes), bf16-exact synthetic"
+    cpu = cpu_measure(args.workload, args.steps, max(1, min(args.warmup, 1)))
     line = {
-        "impl": "reference", "metric": "KV compress+decompress round-trip GB/s (bf16-in)", "value": round(value, 6),
-        "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * total_wall / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (numpy) + u32 (C range coder)", "data": "synthetic",
-        "config": {"workload": args.workload, "name": wl["name"], "tensors": dict(wl["tensors"]),
-                   "shape": list(wl["shape"]), "block_symbols": BLOCK},
-        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": procs, "kind": "port", "sample": sample},
-        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if WORKLOADS[args.workload]["shard"] else "weak", "vs_baseline": None,
+        "dtype": "bf16 in/out; f32/f64 numpy transform+quantizer, u32 C range coder", "data": "synthetic",
+        "config": config_of(args.workload, args.gpus),
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
 
@@ -241,25 +301,16 @@ class ClockSampler:
 # GPU side
 # ----------------------------------------------------------------------------
 
-def main():
-    args = _args()
-    wl = WORKLOADS[args.workload]
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return reference_arm(args, wl, rank)
+def _bits_group(sid: str):
+    w = int(sid.split("b=")[1].split(",")[0]) if "b=" in sid else 4
+    g = int(sid.split("g=")[1].split(",")[0].split(";")[0])
+    return w, g
 
-    # CPU baseline first (fork before any CUDA context exists)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = len(os.sched_getaffinity(0))
-        gbs, nb, wall, tok = cpu_roundtrip(wl, 4 * procs, procs)
-        cpu = {"value": round(gbs, 6), "unit": "GB/s", "cores": procs, "kind": "port",
-               "sample": f"{4 * procs} head slabs x {tok} tokens x {wl['shape'][3]} ch of this workload's strategies, "
-                         f"oracle round trip on {procs} processes ({wall:.1f} s wall)"}
 
-    import numpy as np
+def run_workload(workload: str, args, steps: int, rank: int, world: int, dev, do_e2e: bool,
+                 cpu: dict | None, hbm_peak: float, peak_src: str) -> dict:
+    """Measure one workload on this rank; returns the fields of its JSON line
+    (collectives inside are executed by every rank)."""
     import torch
     import torch.distributed as dist
 
@@ -267,46 +318,33 @@ def main():
     from paper_2605_13734_b200 import _native as N
     from paper_2605_13734_b200.synth import synthetic_kv
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        # keep stdout to the one JSON line (NCCL prints a version banner at VERSION level)
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
-        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[workload]
     shape, (l0, l1) = _shard_shape(wl, rank, world)
     L, H, T, C = shape
     E = L * H * T * C
-
     tensors = []
     for ti, (name, sid) in enumerate(wl["tensors"]):
-        kv, imp = synthetic_kv(L, H, T, C, seed=1000 * rank + 17 * ti + l0, device=dev)
+        kv, _ = synthetic_kv(L, H, T, C, seed=1000 * rank + 17 * ti + l0, device=dev)
         codec = KVCodec(sid, shape, block_symbols=BLOCK, device=dev)
-        blob = codec.alloc_blob()
-        # a 70B 128K cache on one GPU: K, V (2 x 39 GiB) + payloads leave room
-        # for one decode target only -> the tensors share it (serial streams)
-        share = wl["shard"] and world == 1
-        out = tensors[0]["out"] if (share and tensors) else torch.empty_like(kv)
-        tensors.append(dict(name=name, sid=sid, kv=kv, codec=codec, blob=blob, out=out))
-    if wl["shard"] and world == 1:
-        args.streams = 0
+        tensors.append(dict(name=name, sid=sid, kv=kv, codec=codec, blob=codec.alloc_blob(), out=None))
     torch.cuda.synchronize()
     V_rank = 2 * E * len(tensors)  # bf16-in bytes per step on this rank
 
     paged = None
     if wl["paged"]:
-        page_tokens = 16
-        n_pages = T // page_tokens
+        n_pages = T // PAGE_TOKENS
         perm = torch.randperm(n_pages, device=dev).to(torch.int32)
-        paged = dict(page_tokens=page_tokens, table=perm, layer_stride=n_pages * page_tokens * H * C)
+        paged = dict(page_tokens=PAGE_TOKENS, table=perm, layer_stride=n_pages * PAGE_TOKENS * H * C)
         for t in tensors:
-            t["out"] = torch.empty(L * n_pages * page_tokens * H * C, dtype=torch.bfloat16, device=dev)
+            t["out"] = torch.empty(L * n_pages * PAGE_TOKENS * H * C, dtype=torch.bfloat16, device=dev)
+    else:
+        for t in tensors:
+            t["out"] = torch.empty_like(t["kv"])
 
-    # K and V are independent: each runs on its own stream so the HBM-bound
-    # quantize kernels of one overlap the issue-bound range coder of the other
+    # K and V are independent: each runs on its own stream
     main = torch.cuda.current_stream()
     for t in tensors:
-        t["stream"] = torch.cuda.Stream(device=dev) if args.streams else main
+        t["stream"] = main if args.serial else torch.cuda.Stream(device=dev)
 
     def _fork():
         e = torch.cuda.Event()
@@ -331,7 +369,7 @@ def main():
         for t in tensors:
             if paged:
                 t["codec"].decode_paged(t["blob"], t["out"], paged["table"], paged["page_tokens"], paged["layer_stride"],
-                                        stream=t["stream"])
+                                        stream=t["stream"], device_length=True)
             else:
                 t["codec"].decode(t["blob"], out=t["out"], device_length=True, stream=t["stream"])
         _join()
@@ -346,14 +384,14 @@ def main():
         dist.barrier()
 
     # ---------------- timed region
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    clocks = ClockSampler(dev.index)
     time.sleep(0.3)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     wall0 = time.perf_counter()
-    for k in range(args.steps):
+    for k in range(steps):
         ev[k][0].record()
         encode_all()
         ev[k][1].record()
@@ -373,44 +411,39 @@ def main():
         t["codec"].check(decoding=True)
 
     # compressed sizes: the only cross-rank exchange (wire offsets per rank)
-    comp = []
-    for t in tensors:
-        b = t["blob"]
-        comp.append(b.payload_nbytes() + b.metadata.numel() + b.framing_nbytes)
-    comp_rank = sum(comp)
+    comp_rank = sum(t["blob"].payload_nbytes() + t["blob"].metadata.numel() + t["blob"].framing_nbytes for t in tensors)
     if world > 1:
         sizes = torch.zeros(world, dtype=torch.int64, device=dev)
         dist.all_gather_into_tensor(sizes, torch.tensor([comp_rank], dtype=torch.int64, device=dev))
         all_sizes = sizes.tolist()
     else:
         all_sizes = [comp_rank]
-    cr = sum(2 * E for _ in tensors) / sum(t["blob"].compressed_nbytes for t in tensors)
+    cr = V_rank / sum(t["blob"].compressed_nbytes for t in tensors)
     cr_wire = V_rank / comp_rank
 
-    # quality of the round trip (reference quality_score, tensors.py:115-134)
+    # quality of the round trip (reference quality_score, tensors.py:115-134),
+    # squared sums from the fused kvc_sq_error kernel, per layer
     qual = []
     for t in tensors:
-        if t["out"] is tensors[0]["out"] and t is not tensors[0]:
-            t["codec"].decode(t["blob"], out=t["out"], device_length=True)  # shared decode target
-        elif t is tensors[0] and len(tensors) > 1 and tensors[1]["out"] is t["out"]:
-            t["codec"].decode(t["blob"], out=t["out"], device_length=True)
-        se = sx = 0.0
-        for li in range(L):  # per layer: no full-size fp32 temporaries
+        se = torch.zeros((), dtype=torch.float64, device=dev)
+        sx = torch.zeros((), dtype=torch.float64, device=dev)
+        for li in range(L):
             if paged:
                 pg = t["out"].view(L, -1, paged["page_tokens"], H, C)[li, paged["table"].long()]
-                rec = pg.reshape(T, H, C).permute(1, 0, 2).double()
+                rec = pg.reshape(T, H, C).permute(1, 0, 2).contiguous()
             else:
-                rec = t["out"][li].double()
-            x = t["kv"][li].double()
-            se += float(((x - rec) ** 2).sum())
-            sx += float((x * x).sum())
-        rmse, rms = math.sqrt(se / E), math.sqrt(sx / E)
+                rec = t["out"][li]
+            x = t["kv"][li]
+            N.check(N.lib().kvc_sq_error(x.data_ptr(), rec.data_ptr(), x.numel(), N.DTYPE_BF16, se.data_ptr(), None))
+            N.check(N.lib().kvc_sq_error(x.data_ptr(), None, x.numel(), N.DTYPE_BF16, sx.data_ptr(), None))
+        rmse, rms = math.sqrt(float(se) / E), math.sqrt(float(sx) / E)
         qual.append(max(0.0, 1.0 - rmse / rms) if rmse > 1e-9 else 1.0)
 
-    step_ms = total_ms / args.steps
-    value = world * V_rank / (step_ms * 1e-3) / 1e9 if not wl["shard"] else 2 * math.prod(wl["shape"]) * len(tensors) / (step_ms * 1e-3) / 1e9
-    enc_gbs = world * V_rank / (enc_ms / args.steps * 1e-3) / 1e9
-    dec_gbs = world * V_rank / (dec_ms / args.steps * 1e-3) / 1e9
+    step_ms = total_ms / steps
+    V_all = world * V_rank if not wl["shard"] else 2 * math.prod(wl["shape"]) * len(tensors)
+    value = V_all / (step_ms * 1e-3) / 1e9
+    enc_gbs = V_all / (enc_ms / steps * 1e-3) / 1e9
+    dec_gbs = V_all / (dec_ms / steps * 1e-3) / 1e9
 
     # ---------------- per-kernel times (dominant kernel roofline)
     N.profile_enable(True)
@@ -426,149 +459,200 @@ def main():
         t["stream"] = s_
     N.profile_enable(False)
     launches_per_step = sum(c for _, c in prof.values()) / prof_steps
+    alg = {}  # algorithmic bytes per launch for each kernel family
+    for t in tensors:
+        w, g = _bits_group(t["sid"])
+        packed = E * w // 8
+        meta = t["blob"].metadata.numel()
+        coded = t["blob"].payload_nbytes()
+        for k in ("encode_generic", "encode_fast128", "encode_uchan", "decode_generic", "decode_fast128",
+                  "decode_uchan", "decode_delta"):
+            alg.setdefault(k, []).append(2 * E + packed + meta)
+        for k in ("rc_encode", "rc_decode", "rle_encode", "rle_decode"):
+            alg.setdefault(k, []).append(packed + coded)
+        alg.setdefault("gather", []).append(2 * coded)
+        alg.setdefault("fused_encode", []).append(2 * E + coded + meta)
+        alg.setdefault("fused_decode", []).append(2 * E + coded + meta)
+    dom_name, (dom_ms, dom_n) = max(prof.items(), key=lambda kv: kv[1][0])
+    per_launch_ms = dom_ms / dom_n
+    roofline = None
+    if alg.get(dom_name):
+        per_launch_bytes = sum(alg[dom_name]) / len(alg[dom_name])
+        achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        evd = _ncu_evidence(workload, dom_name)
+        roofline = {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 2), "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                    "traffic": round(evd["dram_bytes"]) if evd else None,
+                    "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
+                    "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                    "share_of_step": round(dom_ms / prof_steps / step_ms, 3)}
+        if evd:
+            # instruction roofline: warp-instructions per launch (same capture)
+            # over this run's launch time, against 4 issue slots per SM per cycle
+            roofline["traffic_source"] = evd["source"]
+            roofline["issue"] = {"warp_inst_per_launch": round(evd["inst"]),
+                                 "achieved_tinst_s": round(evd["inst"] / (per_launch_ms * 1e-3) / 1e12, 3),
+                                 "ncu_issue_active_pct": round(evd["issue_pct"], 1)}
+            mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz")
+            if mhz:
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                peak_i = sms * 4 * mhz * 1e6
+                roofline["issue"]["peak_tinst_s"] = round(peak_i / 1e12, 3)
+                roofline["issue"]["frac"] = round(evd["inst"] / (per_launch_ms * 1e-3) / peak_i, 4)
+    step_alg = 2 * sum(2 * E + t["blob"].compressed_nbytes for t in tensors)
+    kernels = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] / prof_steps}
+               for k, v in prof.items()}
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if do_e2e:
+        for t in tensors:  # free the device-resident blobs first (a c3 rank holds 13 GB of them)
+            t["blob"] = None
+        torch.cuda.empty_cache()
+        e2e = measure_e2e(tensors, paged, steps, world, dev, V_all)
+
+    res = {
+        "value": round(value, 3), "unit": "GB/s", "ms_per_step": round(step_ms, 4), "steps": steps,
+        "config": config_of(workload, world),
+        "shape_per_rank": list(shape),
+        "compress_gbs": round(enc_gbs, 3), "decompress_gbs": round(dec_gbs, 3),
+        "compress_hbm_frac": round(enc_gbs * (1 + 1 / cr) / world / hbm_peak, 4),  # per GPU
+        "decompress_hbm_frac": round(dec_gbs * (1 + 1 / cr) / world / hbm_peak, 4),
+        "cr": round(cr, 4), "cr_wire": round(cr_wire, 4), "quality": [round(q, 6) for q in qual],
+        "step_hbm_frac": round(step_alg / (step_ms * 1e-3) / 1e9 / hbm_peak, 4),
+        "roofline": roofline, "kernels": kernels, "gpu_launches": int(round(launches_per_step * steps)),
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "rank_compressed_bytes": all_sizes,
+        "wall_s": round(wall, 3),
+    }
+    del tensors
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_e2e(tensors, paged, steps, world, dev, V_all) -> dict:
+    """Same metric end to end through the public API (hostpath.HostRoundTrip):
+    pinned host KV -> H2D -> encode -> wire into pinned host memory -> H2D ->
+    decode (contiguous or paged) -> D2H of the step's scalar result, pipelined
+    by layer chunks across copy engines, PCIe and SMs."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_13734_b200.hostpath import HostRoundTrip
+
+    host_in = []
+    for t in tensors:
+        h = torch.empty(t["kv"].shape, dtype=t["kv"].dtype, pin_memory=True)
+        h.copy_(t["kv"])
+        host_in.append(h)
+    L_rank = tensors[0]["kv"].shape[0]
+    chunk = max(1, min(8, L_rank // 4)) if L_rank >= 4 else L_rank
+    pg = None if paged is None else (paged["table"], paged["page_tokens"], paged["layer_stride"])
+    rts = [HostRoundTrip(t["sid"], tuple(t["kv"].shape), chunk_layers=chunk, block_symbols=BLOCK, device=dev, paged=pg)
+           for t in tensors]
+    result = torch.zeros((), dtype=torch.float64, device=dev)
+
+    def e2e_step():
+        result.zero_()
+        # the H2D lands in the kv buffers themselves (identical values): no second 42 GB device copy
+        for rt, h, t in zip(rts, host_in, tensors):
+            rt.run(h, t["kv"], t["out"], result)
+        return result.item()  # D2H of the step's result (syncs)
+
+    e2e_step()  # warm-up (plans, pinned buffers)
+    for rt in rts:
+        rt.check()
+    n = max(1, min(3, steps))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(n):
+        e2e_step()
+    s1.record()
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / n
+    wire = sum(rt.wire_bytes() for rt in rts)
+    h2d = sum(h.numel() * 2 for h in host_in) + wire
+    d2h = wire + 8
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    res_kind = "squared reconstruction error (fp64 scalar)" if paged is None else "compressed bytes (paged decode)"
+    out = {"value": round(V_all / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": n, "chunk_layers": chunk,
+           "path": f"pinned host KV -> H2D -> encode -> wire to pinned host -> H2D -> decode -> D2H of the {res_kind} "
+                   "(hostpath.HostRoundTrip, layer-chunk pipeline)"}
+    del rts, host_in
+    return out
+
+
+def main():
+    args = _args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    extras = [] if (args.no_extras or world > 1 or args.workload != "c3") else list(EXTRAS)
+    # CPU baselines first (the worker pools fork before any CUDA context exists)
+    cpus = {}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpus[args.workload] = cpu_measure(args.workload, 2, 1)
+        for w in extras:
+            if w == "c5":
+                cpus[w] = cpu_measure(w, 1, 0)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # algorithmic bytes per launch for each kernel family
-    alg = {}
-    for t in tensors:
-        s = t["sid"]
-        w = int(s.split("b=")[1].split(",")[0]) if "b=" in s else 4
-        g = int(s.split("g=")[1].split(",")[0].split(";")[0])
-        packed = E * w // 8
-        meta = t["blob"].metadata.numel()
-        coded = t["blob"].payload_nbytes()
-        for k in ("encode_generic", "encode_fast128", "encode_uchan"):
-            alg.setdefault(k, []).append(2 * E + packed + meta)
-        for k in ("decode_generic", "decode_fast128", "decode_uchan", "decode_delta"):
-            alg.setdefault(k, []).append(2 * E + packed + meta)
-        alg.setdefault("rc_encode", []).append(packed + coded)
-        alg.setdefault("rc_decode", []).append(packed + coded)
-        alg.setdefault("rle_encode", []).append(packed + coded)
-        alg.setdefault("rle_decode", []).append(packed + coded)
-        alg.setdefault("gather", []).append(2 * coded)
-        # fused quantize + range code: bf16 in, coded blocks + metadata out (and the reverse)
-        alg.setdefault("fused_encode", []).append(2 * E + coded + meta)
-        alg.setdefault("fused_decode", []).append(2 * E + coded + meta)
-    dom = max(prof.items(), key=lambda kv: kv[1][0])
-    dom_name, (dom_ms, dom_n) = dom
-    per_launch_ms = dom_ms / dom_n
-    bytes_list = alg.get(dom_name)
-    roofline = None
-    if bytes_list:
-        per_launch_bytes = sum(bytes_list) / len(bytes_list)
-        achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-        ev = _ncu_evidence(args.workload, dom_name)
-        roofline = {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 2), "peak": hbm_peak,
-                    "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                    "traffic": round(ev["dram_bytes"]) if ev else None,
-                    "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
-                    "share_of_step": round(dom_ms / prof_steps / step_ms, 3)}
-        if ev:
-            # the serial range coders are instruction-bound: warp-instructions
-            # per launch (same capture) over this run's launch time, against
-            # 4 issue slots per SM per cycle at the measured SM clock
-            roofline["traffic_source"] = ev["source"]
-            roofline["issue"] = {"warp_inst_per_launch": round(ev["inst"]),
-                                 "achieved_tinst_s": round(ev["inst"] / (per_launch_ms * 1e-3) / 1e12, 3),
-                                 "ncu_issue_active_pct": round(ev["issue_pct"], 1)}
-            mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz")
-            if mhz:
-                sms = torch.cuda.get_device_properties(dev).multi_processor_count
-                peak_i = sms * 4 * mhz * 1e6
-                roofline["issue"]["peak_tinst_s"] = round(peak_i / 1e12, 3)
-                roofline["issue"]["frac"] = round(ev["inst"] / (per_launch_ms * 1e-3) / peak_i, 4)
-    step_alg = 2 * sum(2 * E + t["blob"].compressed_nbytes for t in tensors)
-    kernels = {k: {"ms_per_step": round(v[0] / prof_steps, 4), "launches_per_step": v[1] / prof_steps} for k, v in prof.items()}
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
 
-    # ---------------- end-to-end through the public API with host buffers
-    # paper_2605_13734_b200.hostpath.HostRoundTrip: pinned host KV -> H2D ->
-    # encode -> wire into pinned host memory -> H2D -> decode, pipelined by
-    # layer chunks across copy engines / PCIe / SMs; the step's result is the
-    # reconstruction squared error, read back to the host.
-    e2e = None
-    if not args.no_e2e and not paged:
-        from paper_2605_13734_b200.hostpath import HostRoundTrip
+    def strip(c):
+        return None if c is None else {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
-        host_in = [t["kv"].cpu().pin_memory() for t in tensors]
-        dev_in = [torch.empty_like(t["kv"]) for t in tensors]
-        L_rank = tensors[0]["kv"].shape[0]
-        chunk = max(1, min(8, L_rank // 4)) if L_rank >= 4 else L_rank
-        rts = [HostRoundTrip(t["sid"], tuple(t["kv"].shape), chunk_layers=chunk, block_symbols=BLOCK, device=dev,
-                             wire_bytes_hint=t["blob"].payload_nbytes()) for t in tensors]
-        outs = [t["out"] for t in tensors]
-        err = torch.zeros((), dtype=torch.float64, device=dev)
-
-        def e2e_step():
-            err.zero_()
-            for rt, h, d_in, o in zip(rts, host_in, dev_in, outs):
-                rt.run(h, d_in, o, err)
-            return err.item()  # D2H of the step's result (syncs)
-
-        e2e_step()  # warm-up (plans, pinned buffers)
-        for rt in rts:
-            rt.check()
-        e2e_steps = max(1, min(3, args.steps))
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for _ in range(e2e_steps):
-            e2e_step()
-        s1.record()
-        torch.cuda.synchronize()
-        e2e_ms = s0.elapsed_time(s1) / e2e_steps
-        wire = sum(rt.wire_bytes() for rt in rts)
-        h2d = sum(h.numel() * 2 for h in host_in) + wire
-        d2h = wire + 8
-        if world > 1:
-            tt = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
-        e2e = {"value": round(world * V_rank / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3),
-               "chunk_layers": chunk,
-               "path": "pinned host KV -> H2D -> encode -> wire to pinned host -> H2D -> decode -> D2H squared-error "
-                       "scalar (hostpath.HostRoundTrip, layer-chunk pipeline)"}
+    head = run_workload(args.workload, args, args.steps, rank, world, dev, not args.no_e2e,
+                        strip(cpus.get(args.workload)), hbm_peak, peak_src)
+    extra = {}
+    for w in extras:
+        extra[w] = run_workload(w, args, EXTRA_STEPS, rank, world, dev, (w == "c5") and not args.no_e2e,
+                                strip(cpus.get(w)), hbm_peak, peak_src)
 
     if rank == 0:
         line = {
-            "metric": "KV compress+decompress round-trip GB/s (bf16-in), s_p = V/(t_enc+t_dec)",
-            "value": round(value, 3),
+            "metric": METRIC,
+            "value": head["value"],
             "unit": "GB/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(step_ms, 4),
+            "ms_per_step": head["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "strong" if wl["shard"] else "weak",
+            "scaling": "strong" if WORKLOADS[args.workload]["shard"] else "weak",
             "vs_baseline": None,
-            "dtype": "bf16 in/out; fp32/fp64 transform+quantizer, u32 range coder",
-            "data": "synthetic (reference generator distribution, rounded to bf16)",
-            "config": {"workload": args.workload, "name": wl["name"], "shape_per_rank": list(shape),
-                       "tensors": dict(wl["tensors"]), "block_symbols": BLOCK,
-                       "l2": "inputs larger than L2 (no flush needed)", "parallelism": f"dp{world} (independent shards)"},
-            "compress_gbs": round(enc_gbs, 3),
-            "decompress_gbs": round(dec_gbs, 3),
-            "cr": round(cr, 4),
-            "cr_wire": round(cr_wire, 4),
-            "quality": [round(q, 6) for q in qual],
-            "step_hbm_frac": round(step_alg / (step_ms * 1e-3) / 1e9 / hbm_peak, 4),
-            "roofline": roofline,
-            "kernels": kernels,
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "clocks": clk,
-            "rank_compressed_bytes": all_sizes,
-            "wall_s": round(wall, 3),
+            "dtype": "bf16 in/out; fp64 Hadamard butterfly, fp32 quantizer, u32 range coder",
+            "data": "synthetic (reference generator distribution, rounded to bf16), generated on the device",
+            "config": head["config"],
         }
+        for k in ("shape_per_rank", "compress_gbs", "decompress_gbs", "compress_hbm_frac", "decompress_hbm_frac", "cr",
+                  "cr_wire", "quality", "step_hbm_frac", "roofline", "kernels", "gpu_launches", "cpu_baseline", "e2e",
+                  "clocks", "rank_compressed_bytes", "wall_s"):
+            line[k] = head[k]
+        if extra:
+            line["extra"] = {w: {k: v for k, v in r.items()} for w, r in extra.items()}
         emit(line)
     if world > 1:
         dist.destroy_process_group()

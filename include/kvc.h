@@ -135,9 +135,10 @@ int kvc_block_crc32(const void* payload, const uint64_t* block_offsets, int64_t 
  * decompress path. */
 int kvc_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes, void* stream);
 
-/* *sum_dev += sum over i < n of (a[i] - b[i])^2 (fp64 accumulation; a, b
- * device arrays of dtype KVC_DTYPE_BF16 or KVC_DTYPE_F32): the quality /
- * error scalar of a round trip (tensors.py:115-134) in one HBM-bound pass. */
+/* *sum_dev += sum over i < n of (a[i] - b[i])^2 (differences, squares and
+ * accumulation in fp64; a, b device arrays of dtype KVC_DTYPE_BF16 or
+ * KVC_DTYPE_F32; b may be NULL for sum a[i]^2): the RMSE / RMS terms of
+ * quality_score (tensors.py:115-134) in one HBM-bound pass each. */
 int kvc_sq_error(const void* a, const void* b, int64_t n, int dtype, double* sum_dev, void* stream);
 
 /* cudaDeviceEnablePeerAccess(peer) from `device` (already-enabled is OK). */

@@ -114,7 +114,9 @@ class KVCodec:
         lib = N.lib()
         handle = ctypes.c_void_p()
         sid = strategy_id.strip() if isinstance(strategy_id, str) else str(strategy_id)
-        N.check(lib.kvc_plan_create(ctypes.byref(handle), sid.encode(), L, H, T, C, ctypes.byref(opts)))
+        # the plan (SM count, range-coder tables) belongs to self.device
+        with torch.cuda.device(self.device):
+            N.check(lib.kvc_plan_create(ctypes.byref(handle), sid.encode(), L, H, T, C, ctypes.byref(opts)))
         self._h = handle
         self._lib = lib
         self.strategy_id = lib.kvc_plan_strategy_id(handle).decode()
@@ -158,6 +160,16 @@ class KVCodec:
             offsets = torch.zeros(self.max_blocks + 1, dtype=torch.int64, device=dev)
         cls = None if head_classes is None else np.asarray(head_classes, dtype=bool).reshape(self.shape[:2])
         return DeviceBlob(payload, meta, offsets, self.strategy_id, self.shape, cls)
+
+    def num_blocks(self, blob: DeviceBlob | None = None, head_classes=None) -> int:
+        """Codec blocks of an encode with these head labels (0 for c=none)."""
+        cls = head_classes if head_classes is not None else (None if blob is None else blob.head_classes)
+        if self.needs_classes and cls is None:
+            raise ValueError("mixed_head quantization needs head labels to count blocks")
+        arr, cptr = self._classes_arg(cls) if self.needs_classes else (None, None)
+        n = int(self._lib.kvc_num_blocks(self._h, cptr))
+        del arr
+        return n
 
     # ------------------------------------------------------------- encode
     def encode(self, kv: torch.Tensor, head_classes=None, out: DeviceBlob | None = None,
@@ -205,14 +217,22 @@ class KVCodec:
         return out
 
     def decode_paged(self, blob: DeviceBlob, pages: torch.Tensor, block_table: torch.Tensor, page_tokens: int,
-                     layer_stride: int, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-        """Decode into a paged cache (vLLM layout [pages, page_tokens, H, C] per layer)."""
+                     layer_stride: int, stream: torch.cuda.Stream | None = None,
+                     device_length: bool = False) -> torch.Tensor:
+        """Decode into a paged cache (vLLM layout [pages, page_tokens, H, C] per
+        layer).  device_length=True: payload length from the device offset
+        table (no host sync)."""
         if pages.dtype != self.out_dtype:
             raise ValueError("page dtype must match the plan's out_dtype")
-        bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
+        if blob.metadata.numel() != self.metadata_bytes:
+            raise N.CodecError(f"metadata is {blob.metadata.numel()} bytes, expected {self.metadata_bytes}")
+        bt = block_table
+        if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
+            bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
+        nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
         N.check(
             self._lib.kvc_decode_paged(
-                self._h, blob.payload.data_ptr(), blob.payload_nbytes(), blob.metadata.data_ptr(), _ptr(blob.offsets),
+                self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),
                 pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), self.workspace.data_ptr(),
                 _stream_handle(stream),
             )

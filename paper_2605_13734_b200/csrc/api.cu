@@ -11,6 +11,7 @@
 
 #include "kernels.h"
 #include "kvc_internal.h"
+#include "rc_tables.cuh"
 
 using namespace kvc;
 
@@ -278,6 +279,16 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   }
   p.ws_bytes = off;
   snprintf(p.id, sizeof p.id, "%s", canon.c_str());
+  // the range coders' reciprocal tables: built (synchronously) now, so no
+  // coder on any stream or inside a captured graph can run ahead of them
+  if (g.codec == C_ENTROPY) {
+    cudaError_t te = ensure_recip_tables();
+    if (te == cudaErrorNoDevice || te == cudaErrorInsufficientDriver) {
+      cudaGetLastError();  // size queries work without a GPU; launches retry and fail loudly
+    } else if (te != cudaSuccess) {
+      return cuda_fail(te, "range-coder tables");
+    }
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
@@ -570,7 +581,7 @@ int kvc_enable_peer_access(int device, int peer) {
 
 int kvc_sq_error(const void* a, const void* b, int64_t n, int dtype, double* sum_dev, void* stream) {
   if (n <= 0) return KVC_OK;
-  if (!a || !b || !sum_dev) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  if (!a || !sum_dev) return fail(KVC_ERR_CONFIG, "NULL buffer");
   if (dtype != KVC_DTYPE_BF16 && dtype != KVC_DTYPE_F32) return fail(KVC_ERR_CONFIG, "dtype must be bf16 or f32");
   if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) != 0)
     return fail(KVC_ERR_CONFIG, "inputs must be 16-byte aligned");

@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
   const int64_t n = min(a.g.block, st.count[si] - start);
   const int64_t want = (n * w + 7) / 8;
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  if (o1 < o0 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
+  // PackBits grows a block by at most one control byte per 128 literals
+  if (o1 < o0 || o1 - o0 > (uint64_t)(want + want / 64 + 16) ||
+      (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
@@ -319,7 +321,10 @@ size_t codec_scan_bytes(int64_t max_blocks) {
 cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_t s) {
   (void)sm_count;
   CodecArgs a = args;
-  if (a.g.codec == C_ENTROPY) a.recip = recip_tables(s);
+  if (a.g.codec == C_ENTROPY) {
+    if (cudaError_t te = ensure_recip_tables(); te != cudaSuccess) return te;
+    a.recip = recip_tables();
+  }
   const unsigned grid = (unsigned)((a.max_blocks + 1 + 127) / 128);
   bool used[9];
   widths_used(a.g, used);
@@ -367,7 +372,10 @@ cudaError_t launch_check_payload(const CodecArgs& a, cudaStream_t s) {
 cudaError_t launch_codec_decode(const CodecArgs& args, int sm_count, cudaStream_t s) {
   (void)sm_count;
   CodecArgs a = args;
-  if (a.g.codec == C_ENTROPY) a.recip = recip_tables(s);
+  if (a.g.codec == C_ENTROPY) {
+    if (cudaError_t te = ensure_recip_tables(); te != cudaSuccess) return te;
+    a.recip = recip_tables();
+  }
   cudaError_t ce = launch_check_payload(a, s);
   if (ce != cudaSuccess || a.g.codec == C_NONE) return ce;
   const unsigned grid = (unsigned)((a.max_blocks + 127) / 128 + 1);
@@ -470,7 +478,14 @@ cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t
 }
 
 // ------------------------------------------------------ squared error sum
-template <typename T>
+// sum((a - b)^2) (b == nullptr: sum(a^2)) with every difference and square in
+// fp64 (exact differences, like tensors.py:126's astype(float64) - ...), fp64
+// accumulation; only the summation order differs from numpy's pairwise mean
+__device__ __forceinline__ double sq_term(float a, float b) {
+  const double d = (double)a - (double)b;
+  return d * d;
+}
+template <typename T, bool HAS_B>
 __global__ void __launch_bounds__(256) k_sq_error(const T* a, const T* b, int64_t n, double* out) {
   constexpr int kVec = 16 / sizeof(T);
   const int64_t nv = n / kVec;
@@ -480,32 +495,29 @@ __global__ void __launch_bounds__(256) k_sq_error(const T* a, const T* b, int64_
   const uint4* a4 = reinterpret_cast<const uint4*>(a);
   const uint4* b4 = reinterpret_cast<const uint4*>(b);
   for (int64_t i = tid; i < nv; i += stride) {
-    const uint4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+    const uint4 x = __ldg(a4 + i);
+    const uint4 y = HAS_B ? __ldg(b4 + i) : make_uint4(0u, 0u, 0u, 0u);
     const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
-    float part = 0.0f;  // <= 8 terms in fp32, then fp64
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if constexpr (sizeof(T) == 2) {
-        const float d0 = __uint_as_float(xw[k] << 16) - __uint_as_float(yw[k] << 16);
-        const float d1 = __uint_as_float(xw[k] & 0xFFFF0000u) - __uint_as_float(yw[k] & 0xFFFF0000u);
-        part = __fmaf_rn(d0, d0, __fmaf_rn(d1, d1, part));
+        acc += sq_term(__uint_as_float(xw[k] << 16), __uint_as_float(yw[k] << 16));
+        acc += sq_term(__uint_as_float(xw[k] & 0xFFFF0000u), __uint_as_float(yw[k] & 0xFFFF0000u));
       } else {
-        const float d = __uint_as_float(xw[k]) - __uint_as_float(yw[k]);
-        part = __fmaf_rn(d, d, part);
+        acc += sq_term(__uint_as_float(xw[k]), __uint_as_float(yw[k]));
       }
     }
-    acc += (double)part;
   }
   for (int64_t i = nv * kVec + tid; i < n; i += stride) {
-    float fa, fb;
+    float fa, fb = 0.0f;
     if constexpr (sizeof(T) == 2) {
       fa = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(a)[i] << 16);
-      fb = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(b)[i] << 16);
+      if (HAS_B) fb = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(b)[i] << 16);
     } else {
       fa = reinterpret_cast<const float*>(a)[i];
-      fb = reinterpret_cast<const float*>(b)[i];
+      if (HAS_B) fb = reinterpret_cast<const float*>(b)[i];
     }
-    acc += (double)(fa - fb) * (double)(fa - fb);
+    acc += sq_term(fa, fb);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -527,10 +539,17 @@ cudaError_t launch_sq_error(const void* a, const void* b, int64_t n, int dtype, 
   const int64_t cap = (int64_t)sms * 8;
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   ProfScope ps("sq_error", s);
-  if (dtype == KVC_DTYPE_BF16)
-    k_sq_error<uint16_t><<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(a), reinterpret_cast<const uint16_t*>(b), n, out);
-  else
-    k_sq_error<float><<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(a), reinterpret_cast<const float*>(b), n, out);
+  const uint16_t* ah = reinterpret_cast<const uint16_t*>(a);
+  const uint16_t* bh = reinterpret_cast<const uint16_t*>(b);
+  const float* af = reinterpret_cast<const float*>(a);
+  const float* bf = reinterpret_cast<const float*>(b);
+  if (dtype == KVC_DTYPE_BF16) {
+    if (b) k_sq_error<uint16_t, true><<<grid, 256, 0, s>>>(ah, bh, n, out);
+    else k_sq_error<uint16_t, false><<<grid, 256, 0, s>>>(ah, bh, n, out);
+  } else {
+    if (b) k_sq_error<float, true><<<grid, 256, 0, s>>>(af, bf, n, out);
+    else k_sq_error<float, false><<<grid, 256, 0, s>>>(af, bf, n, out);
+  }
   return cudaGetLastError();
 }
 

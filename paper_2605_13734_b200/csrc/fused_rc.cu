@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedAr
 // which then decodes a zero stream (so warp-cooperative stores stay intact)
 __device__ __forceinline__ bool open_block(const FusedArgs& a, int64_t b, RcDec& d, int64_t& avail) {
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  bool ok = o1 >= o0 + 8 && (a.payload_bytes < 0 || (int64_t)o1 <= a.payload_bytes);
+  bool ok = o1 >= o0 && o1 - o0 >= 8 && (a.payload_bytes < 0 || (int64_t)o1 <= a.payload_bytes);
   if (ok) {
     const uint8_t* src = a.payload_in + o0;
     const uint32_t hdr = ((uint32_t)src[0] << 24) | ((uint32_t)src[1] << 16) | ((uint32_t)src[2] << 8) | src[3];
@@ -606,28 +606,15 @@ bool fused_rc_applicable_impl(const Geo& g) {
   return g.E < (1ll << 40);
 }
 
-std::mutex g_const_mu;
-bool g_const_ready[64];
-
-// copy rows w = 1..4 of the device reciprocal tables into c_recip once per device
-cudaError_t ensure_const_tables(cudaStream_t s) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_const_mu);
-  if (dev < 0 || dev >= 64 || g_const_ready[dev]) return cudaSuccess;
-  const uint32_t* rt = recip_tables(s);
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_recip, rt + kRecipLen, sizeof(c_recip), 0, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) g_const_ready[dev] = true;
-  return e;
-}
-
 }  // namespace
+
+cudaError_t upload_fused_recip(const uint32_t* rows) { return cudaMemcpyToSymbol(c_recip, rows, sizeof(c_recip)); }
 
 bool fused_rc_applicable(const Geo& g) { return fused_rc_applicable_impl(g); }
 
 cudaError_t launch_fused_rc_encode(const FusedArgs& args, cudaStream_t s) {
   FusedArgs a = args;
-  cudaError_t ce = ensure_const_tables(s);
+  cudaError_t ce = ensure_recip_tables();
   if (ce != cudaSuccess) return ce;
   ProfScope ps("fused_encode", s);
   switch (a.g.bits) {
@@ -640,7 +627,7 @@ cudaError_t launch_fused_rc_encode(const FusedArgs& args, cudaStream_t s) {
 
 cudaError_t launch_fused_rc_decode(const FusedArgs& args, cudaStream_t s) {
   FusedArgs a = args;
-  cudaError_t ce = ensure_const_tables(s);
+  cudaError_t ce = ensure_recip_tables();
   if (ce != cudaSuccess) return ce;
   ProfScope ps("fused_decode", s);
   return a.g.out_dtype == KVC_DTYPE_BF16 ? dec_t<__nv_bfloat16>(a, s) : dec_t<float>(a, s);

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kLThreads) k_rc_large_decode(CodecArgs a) {
   const int64_t start = (b - st.first_block[si]) * a.g.block;
   const int n = (int)min(a.g.block, st.count[si] - start);
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  if (o1 < o0 + 8 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
+  if (o1 < o0 || o1 - o0 < 8 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
@@ -412,26 +412,14 @@ cudaError_t dec_w(const CodecArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-std::mutex g_lconst_mu;
-bool g_lconst_ready[64];
-
-// copy rows w = 5..8 of the device reciprocal tables into c_recip_l once per device
-cudaError_t ensure_lconst_tables(cudaStream_t s) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_lconst_mu);
-  if (dev < 0 || dev >= 64 || g_lconst_ready[dev]) return cudaSuccess;
-  const uint32_t* rt = recip_tables(s);
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_recip_l, rt + 5 * kRecipLen, sizeof(c_recip_l), 0,
-                                          cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) g_lconst_ready[dev] = true;
-  return e;
-}
-
 }  // namespace
 
+cudaError_t upload_large_recip(const uint32_t* rows) {
+  return cudaMemcpyToSymbol(c_recip_l, rows, sizeof(c_recip_l));
+}
+
 cudaError_t launch_rc_large_encode(const CodecArgs& a, int w, cudaStream_t s) {
-  if (cudaError_t ce = ensure_lconst_tables(s); ce != cudaSuccess) return ce;
+  if (cudaError_t ce = ensure_recip_tables(); ce != cudaSuccess) return ce;
   ProfScope ps("rc_encode", s);
   switch (w) {
     case 5: return enc_w<5>(a, s);
@@ -442,7 +430,7 @@ cudaError_t launch_rc_large_encode(const CodecArgs& a, int w, cudaStream_t s) {
 }
 
 cudaError_t launch_rc_large_decode(const CodecArgs& a, int w, cudaStream_t s) {
-  if (cudaError_t ce = ensure_lconst_tables(s); ce != cudaSuccess) return ce;
+  if (cudaError_t ce = ensure_recip_tables(); ce != cudaSuccess) return ce;
   ProfScope ps("rc_decode", s);
   switch (w) {
     case 5: return dec_w<5>(a, s);

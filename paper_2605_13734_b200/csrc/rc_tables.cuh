@@ -13,9 +13,15 @@ namespace kvc {
 
 constexpr int kRecipLen = 2048;  // >= ceil((65536 - A) / 32) for every A >= 2
 
-// device pointer to the [9][kRecipLen] table (row w = alphabet 2^w); builds
-// it on first use for the current device (stream-ordered on `s`)
-const uint32_t* recip_tables(cudaStream_t s);
+// Build the tables on the current device once (host-computed, synchronous
+// copy + device synchronize; a lock + flag test afterwards).  kvc_plan_create
+// calls it for entropy plans; the launch paths call it again as a guard.
+cudaError_t ensure_recip_tables();
+// device pointer to the [9][kRecipLen] table (row w = alphabet 2^w)
+const uint32_t* recip_tables();
+// rows w = 1..4 / 5..8 into the coders' __constant__ copies (synchronous)
+cudaError_t upload_fused_recip(const uint32_t* rows_1_to_4);
+cudaError_t upload_large_recip(const uint32_t* rows_5_to_8);
 
 __device__ __forceinline__ uint32_t div_recip(uint32_t n, uint32_t d, uint32_t m) {
   // floor(n / d) given m = floor(2^32 / d): the product estimate is q or q-1

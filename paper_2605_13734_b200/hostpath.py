@@ -33,18 +33,20 @@ __all__ = ["HostRoundTrip"]
 
 class HostRoundTrip:
     def __init__(self, strategy_id: str, shape, chunk_layers: int = 4, block_symbols: int = 2048, device=None,
-                 wire_bytes_hint: int | None = None) -> None:
+                 paged=None) -> None:
+        """paged = (block_table int32 cuda, page_tokens, layer_stride): decode
+        into a paged cache (kvc_decode_paged; one table shared by every
+        layer, `out` the page pool of all layers) instead of a contiguous
+        (L, H, T, C) tensor."""
         L, H, T, C = (int(v) for v in shape)
         self.shape = (L, H, T, C)
+        self.paged = paged
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.chunks = [(l0, min(L, l0 + chunk_layers)) for l0 in range(0, L, chunk_layers)]
         enc_plans: dict[int, KVCodec] = {}
         dec_plans: dict[int, KVCodec] = {}
         self.enc, self.dec, self.blob, self.rx = [], [], [], []
         self.h_pay, self.h_meta, self.h_off = [], [], []
-        per_chunk_hint = None
-        if wire_bytes_hint is not None:
-            per_chunk_hint = int(wire_bytes_hint * chunk_layers / L * 1.1) + (1 << 16)
         with torch.cuda.device(self.device):
             for l0, l1 in self.chunks:
                 n = l1 - l0
@@ -56,11 +58,12 @@ class HostRoundTrip:
                 self.dec.append(d)
                 self.blob.append(e.alloc_blob())
                 self.rx.append(d.alloc_blob())
-                cap = e.payload_capacity if per_chunk_hint is None else min(e.payload_capacity, per_chunk_hint)
-                self.h_pay.append(torch.empty(max(cap, 16), dtype=torch.uint8).pin_memory())
-                self.h_meta.append(torch.empty(max(e.metadata_bytes, 1), dtype=torch.uint8).pin_memory())
+                # the full payload capacity: the device-length copy can never
+                # truncate a chunk (a shorter buffer would drop bytes silently)
+                self.h_pay.append(torch.empty(max(e.payload_capacity, 16), dtype=torch.uint8, pin_memory=True))
+                self.h_meta.append(torch.empty(max(e.metadata_bytes, 1), dtype=torch.uint8, pin_memory=True))
                 self.h_off.append(None if e.codec_kind == "none" else
-                                  torch.zeros(e.max_blocks + 1, dtype=torch.int64).pin_memory())
+                                  torch.zeros(e.max_blocks + 1, dtype=torch.int64, pin_memory=True))
             mk = lambda: torch.cuda.Stream(self.device)  # noqa: E731
             self.s_in, self.s_enc, self.s_out, self.s_back, self.s_dec = mk(), mk(), mk(), mk(), mk()
             ev = lambda: [torch.cuda.Event() for _ in self.chunks]  # noqa: E731
@@ -130,8 +133,16 @@ class HostRoundTrip:
                 rx.nblocks, rx._nbytes = blob.nblocks, blob._nbytes
                 # decode + error
                 self.s_dec.wait_event(self.e_back[i])
-                dec.decode(rx, out=out[l0:l1], stream=self.s_dec, device_length=ho is not None)
-                if err_sum is not None:
+                if self.paged is not None:
+                    table, page_tokens, stride = self.paged
+                    dec.decode_paged(rx, out[l0 * stride:l1 * stride], table, page_tokens, stride, stream=self.s_dec,
+                                     device_length=ho is not None)
+                    if err_sum is not None and ho is not None:  # the step's scalar: compressed bytes
+                        with torch.cuda.stream(self.s_dec):
+                            err_sum.add_(rx.offsets[rx.nblocks].to(torch.float64))
+                else:
+                    dec.decode(rx, out=out[l0:l1], stream=self.s_dec, device_length=ho is not None)
+                if err_sum is not None and self.paged is None:
                     n = (l1 - l0) * self.shape[1] * self.shape[2] * self.shape[3]
                     dt = N.DTYPE_BF16 if out.dtype == torch.bfloat16 else N.DTYPE_F32
                     N.check(lib.kvc_sq_error(out[l0:l1].data_ptr(), dev_in[l0:l1].data_ptr(), n, dt,

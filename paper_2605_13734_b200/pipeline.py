@@ -140,7 +140,12 @@ class CompressedBlob:
 
     @property
     def cr(self) -> float:
-        """Wire ratio: original / (payload + metadata + block table)."""
+        """Reference accounting: original / (payload + metadata) (codecs.py:69-71)."""
+        return self.original_bytes / self.compressed_nbytes
+
+    @property
+    def cr_wire(self) -> float:
+        """Wire ratio including the block table needed for parallel decode."""
         return self.original_bytes / (self.compressed_nbytes + self.framing_nbytes)
 
 
@@ -275,18 +280,35 @@ def _as_device_values(x, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(device)
 
 
+def _sum_sq(a: torch.Tensor, b: torch.Tensor | None) -> float:
+    """sum((a - b)^2) (b None: sum(a^2)) in fp64 through kvc_sq_error: one
+    HBM-bound pass, no full-size fp64 temporaries."""
+    a = a.contiguous()
+    b = None if b is None else b.contiguous()
+    acc = torch.zeros((), dtype=torch.float64, device=a.device)
+    dt = N.DTYPE_BF16 if a.dtype == torch.bfloat16 else N.DTYPE_F32
+    N.check(N.lib().kvc_sq_error(a.data_ptr(), None if b is None else b.data_ptr(), a.numel(), dt, acc.data_ptr(),
+                                 torch.cuda.current_stream(a.device).cuda_stream or None))
+    return float(acc.item())
+
+
 def quality_score(original, reconstructed) -> float:
-    """max(0, 1 - RMSE/RMS) in float64 (tensors.py:115-134), on the device."""
+    """max(0, 1 - RMSE/RMS) in float64 (tensors.py:115-134), on the device:
+    the squared error and the squared norm are fp64 sums from the fused
+    kvc_sq_error kernel (per-element differences are exact in fp32 for
+    bf16/fp32 inputs of one dtype)."""
     dev = torch.device("cuda", torch.cuda.current_device())
-    a = _as_device_values(original, dev).double()
-    b = _as_device_values(reconstructed, dev).double()
+    a = _as_device_values(original, dev)
+    b = _as_device_values(reconstructed, dev)
     if a.shape != b.shape:
         raise ValueError(f"shape mismatch: {tuple(a.shape)} vs {tuple(b.shape)}")
-    d = a - b
-    rmse = math.sqrt(float(torch.mean(d * d)))
+    if a.dtype != b.dtype or a.dtype not in (torch.bfloat16, torch.float32):
+        a, b = a.float(), b.float()
+    n = a.numel()
+    rmse = math.sqrt(_sum_sq(a, b) / n)
     if rmse <= 1e-9:
         return 1.0
-    rms = math.sqrt(float(torch.mean(a * a)))
+    rms = math.sqrt(_sum_sq(a, None) / n)
     if rms == 0.0:
         return 0.0
     return max(0.0, 1.0 - rmse / rms)
@@ -370,10 +392,21 @@ def compress(x, s, timer: StageTimer | None = None, block_symbols: int = 2048):
         head_importance=x.head_importance,
         block_offsets=dblob.offsets_array(),
         strategy_id=s.id,
-        device=dblob,
+        device=_trimmed(dblob),
     )
     metrics = PipelineMetrics(cr=blob.cr, s_enc=nbytes / enc_s, s_dec=nbytes / dec_s, quality=quality_score(v, rec))
     return blob, metrics
+
+
+def _trimmed(d: DeviceBlob) -> DeviceBlob:
+    """The blob with its payload cut to the bytes actually written (the
+    encode buffer is capacity-sized: ~4 B per symbol for entropy)."""
+    n = d.payload_nbytes()
+    offs = None if d.offsets is None else d.offsets[: d.nblocks + 1].clone()
+    t = DeviceBlob(d.payload[: max(n, 1)].clone(), d.metadata.clone(), offs, d.strategy_id, d.shape, d.head_classes,
+                   d.nblocks)
+    t._nbytes = n
+    return t
 
 
 def _check_blob_matches(blob, s: StrategyConfig) -> None:
@@ -390,6 +423,22 @@ def _check_blob_matches(blob, s: StrategyConfig) -> None:
     sid = getattr(blob, "strategy_id", "")
     if sid and sid != s.id:
         raise CodecError(f"blob was encoded with {sid!r}, not {s.id!r}")
+
+
+def _checked_offsets(offsets, payload_len: int, nblocks: int) -> np.ndarray:
+    """Validate a host block table before it reaches the device: starts at 0,
+    ends at the payload length, never decreases, one entry per block + 1."""
+    o = np.asarray(offsets)
+    if o.ndim != 1 or o.dtype.kind not in "iu":
+        raise CodecError("block offsets must be a 1-D integer array")
+    o = o.astype(np.int64)
+    if o.size != nblocks + 1:
+        raise CodecError(f"block table has {o.size - 1} blocks, expected {nblocks}")
+    if o[0] != 0 or o[-1] != payload_len:
+        raise CodecError(f"block offsets span [{o[0]}, {o[-1]}], payload is {payload_len} bytes")
+    if np.any(np.diff(o) < 0):
+        raise CodecError("block offsets decrease")
+    return np.ascontiguousarray(o)
 
 
 def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_symbols: int = 2048):
@@ -412,9 +461,13 @@ def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_s
         dblob.payload[: pay.size].copy_(torch.from_numpy(pay.copy()))
         dblob.metadata.copy_(torch.from_numpy(meta.copy()))
         if blob.block_offsets is not None:
-            offs = torch.from_numpy(np.asarray(blob.block_offsets, dtype=np.int64))
+            cls = (np.asarray(blob.bits_per_head) == s.quant.high_bits) if blob.mixed else None
+            offs_np = _checked_offsets(blob.block_offsets, pay.size, codec.num_blocks(head_classes=cls))
+            offs = torch.from_numpy(offs_np)
             dblob.offsets[: offs.numel()].copy_(offs)
             dblob.nblocks = offs.numel() - 1
+        elif codec.codec_kind != "none":
+            raise CodecError("rle/entropy blob without a block offset table")
         dblob._nbytes = pay.size
     else:
         codec = _plan(s.id, blob.shape, torch.bfloat16, block_symbols)

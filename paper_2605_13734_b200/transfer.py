@@ -98,7 +98,14 @@ class PipelinedKVTransfer:
         if out is None:
             out = torch.empty(self.shape, dtype=self.out_dtype, device=self.dst)
         cur_src = torch.cuda.current_stream(self.src)
+        cur_dst = torch.cuda.current_stream(self.dst)
+        # work already queued by the caller: kv's producer on the source, and
+        # any pending use of `out` (a reused KV slot) on the destination
         self.s_enc.wait_stream(cur_src)
+        self.s_copy.wait_stream(cur_dst)
+        self.s_dec.wait_stream(cur_dst)
+        kv.record_stream(self.s_enc)
+        out.record_stream(self.s_dec)
         for i, (l0, l1) in enumerate(self.chunks):
             cls = None if head_classes is None else head_classes[l0:l1]
             src_blob, dst_blob = self.tx_src[i], self.tx_dst[i]
@@ -126,7 +133,10 @@ class PipelinedKVTransfer:
                 self.dec[i].decode(dst_blob, out=out[l0:l1], stream=self.s_dec,
                                    device_length=dst_blob.offsets is not None)
                 self.ev_dec[i].record(self.s_dec)
-        torch.cuda.current_stream(self.dst).wait_stream(self.s_dec)
+        cur_dst.wait_stream(self.s_dec)
+        # the caller may free or overwrite kv once its own stream moves on
+        cur_src.wait_stream(self.s_enc)
+        cur_src.wait_stream(self.s_copy)
         return out
 
     def check(self) -> None:
