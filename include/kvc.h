@@ -141,6 +141,14 @@ int kvc_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_de
  * quality_score (tensors.py:115-134) in one HBM-bound pass each. */
 int kvc_sq_error(const void* a, const void* b, int64_t n, int dtype, double* sum_dev, void* stream);
 
+/* Deterministic form of kvc_sq_error: npartials CTAs (1..65535) with a fixed
+ * work split and reduction order; CTA i adds its share to partials[i] (device,
+ * npartials doubles).  Summing the partials in order gives the same bits on
+ * every call (the quality_score of the profiling evaluator must be a function
+ * of its inputs, search.py:348-368). */
+int kvc_sq_error_partials(const void* a, const void* b, int64_t n, int dtype, double* partials, int64_t npartials,
+                          void* stream);
+
 /* cudaDeviceEnablePeerAccess(peer) from `device` (already-enabled is OK). */
 int kvc_enable_peer_access(int device, int peer);
 

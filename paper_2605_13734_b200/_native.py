@@ -43,6 +43,7 @@ EXPORTS = (
     "kvc_copy_device_length",
     "kvc_enable_peer_access",
     "kvc_sq_error",
+    "kvc_sq_error_partials",
 )
 
 
@@ -111,6 +112,8 @@ def lib() -> ctypes.CDLL:
     L.kvc_enable_peer_access.restype = I32
     L.kvc_sq_error.argtypes = [P, P, I64, I32, P, P]
     L.kvc_sq_error.restype = I32
+    L.kvc_sq_error_partials.argtypes = [P, P, I64, I32, P, I64, P]
+    L.kvc_sq_error_partials.restype = I32
     _lib = L
     return L
 

@@ -590,6 +590,19 @@ int kvc_sq_error(const void* a, const void* b, int64_t n, int dtype, double* sum
   return KVC_OK;
 }
 
+int kvc_sq_error_partials(const void* a, const void* b, int64_t n, int dtype, double* partials, int64_t npartials,
+                          void* stream) {
+  if (n <= 0) return KVC_OK;
+  if (!a || !partials) return fail(KVC_ERR_CONFIG, "NULL buffer");
+  if (npartials < 1 || npartials > 65535) return fail(KVC_ERR_CONFIG, "npartials must be in 1..65535");
+  if (dtype != KVC_DTYPE_BF16 && dtype != KVC_DTYPE_F32) return fail(KVC_ERR_CONFIG, "dtype must be bf16 or f32");
+  if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15u) != 0)
+    return fail(KVC_ERR_CONFIG, "inputs must be 16-byte aligned");
+  cudaError_t e = launch_sq_error_partials(a, b, n, dtype, partials, npartials, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "sq_error");
+  return KVC_OK;
+}
+
 int kvc_read_status(const kvc_plan* plan, void* workspace, void* stream, uint32_t* flags) {
   if (!plan || !workspace || !flags) return fail(KVC_ERR_CONFIG, "NULL argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -485,7 +485,9 @@ __device__ __forceinline__ double sq_term(float a, float b) {
   const double d = (double)a - (double)b;
   return d * d;
 }
-template <typename T, bool HAS_B>
+// PARTIALS: block i adds its sum to out[i] (fixed work split and fixed
+// reduction order: deterministic); else every block atomically adds to out[0]
+template <typename T, bool HAS_B, bool PARTIALS = false>
 __global__ void __launch_bounds__(256) k_sq_error(const T* a, const T* b, int64_t n, double* out) {
   constexpr int kVec = 16 / sizeof(T);
   const int64_t nv = n / kVec;
@@ -527,7 +529,8 @@ __global__ void __launch_bounds__(256) k_sq_error(const T* a, const T* b, int64_
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
-    atomicAdd(out, t);
+    if (PARTIALS) out[blockIdx.x] += t;
+    else atomicAdd(out, t);
   }
 }
 
@@ -549,6 +552,24 @@ cudaError_t launch_sq_error(const void* a, const void* b, int64_t n, int dtype, 
   } else {
     if (b) k_sq_error<float, true><<<grid, 256, 0, s>>>(af, bf, n, out);
     else k_sq_error<float, false><<<grid, 256, 0, s>>>(af, bf, n, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sq_error_partials(const void* a, const void* b, int64_t n, int dtype, double* partials,
+                                     int64_t npartials, cudaStream_t s) {
+  const unsigned grid = (unsigned)npartials;
+  ProfScope ps("sq_error", s);
+  const uint16_t* ah = reinterpret_cast<const uint16_t*>(a);
+  const uint16_t* bh = reinterpret_cast<const uint16_t*>(b);
+  const float* af = reinterpret_cast<const float*>(a);
+  const float* bf = reinterpret_cast<const float*>(b);
+  if (dtype == KVC_DTYPE_BF16) {
+    if (b) k_sq_error<uint16_t, true, true><<<grid, 256, 0, s>>>(ah, bh, n, partials);
+    else k_sq_error<uint16_t, false, true><<<grid, 256, 0, s>>>(ah, bh, n, partials);
+  } else {
+    if (b) k_sq_error<float, true, true><<<grid, 256, 0, s>>>(af, bf, n, partials);
+    else k_sq_error<float, false, true><<<grid, 256, 0, s>>>(af, bf, n, partials);
   }
   return cudaGetLastError();
 }

@@ -151,6 +151,8 @@ cudaError_t launch_check_payload(const CodecArgs& a, cudaStream_t s);
 cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t* nbytes_dev, int64_t max_bytes,
                                       cudaStream_t s);
 cudaError_t launch_sq_error(const void* a, const void* b, int64_t n, int dtype, double* out, cudaStream_t s);
+cudaError_t launch_sq_error_partials(const void* a, const void* b, int64_t n, int dtype, double* partials,
+                                     int64_t npartials, cudaStream_t s);
 cudaError_t launch_block_crc32(const uint8_t* payload, const uint64_t* offsets, int64_t nblocks, uint32_t* crc,
                                cudaStream_t s);
 

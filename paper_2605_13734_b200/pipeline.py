@@ -280,16 +280,21 @@ def _as_device_values(x, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(device)
 
 
+_SQ_PARTIALS = 592  # CTAs of the deterministic squared-sum kernel (4 per SM)
+
+
 def _sum_sq(a: torch.Tensor, b: torch.Tensor | None) -> float:
-    """sum((a - b)^2) (b None: sum(a^2)) in fp64 through kvc_sq_error: one
-    HBM-bound pass, no full-size fp64 temporaries."""
+    """sum((a - b)^2) (b None: sum(a^2)) in fp64 through kvc_sq_error_partials:
+    one HBM-bound pass, no full-size fp64 temporaries, and the same bits on
+    every call (fixed work split and reduction order)."""
     a = a.contiguous()
     b = None if b is None else b.contiguous()
-    acc = torch.zeros((), dtype=torch.float64, device=a.device)
+    part = torch.zeros(_SQ_PARTIALS, dtype=torch.float64, device=a.device)
     dt = N.DTYPE_BF16 if a.dtype == torch.bfloat16 else N.DTYPE_F32
-    N.check(N.lib().kvc_sq_error(a.data_ptr(), None if b is None else b.data_ptr(), a.numel(), dt, acc.data_ptr(),
-                                 torch.cuda.current_stream(a.device).cuda_stream or None))
-    return float(acc.item())
+    N.check(N.lib().kvc_sq_error_partials(a.data_ptr(), None if b is None else b.data_ptr(), a.numel(), dt,
+                                          part.data_ptr(), _SQ_PARTIALS,
+                                          torch.cuda.current_stream(a.device).cuda_stream or None))
+    return float(np.sum(part.cpu().numpy()))
 
 
 def quality_score(original, reconstructed) -> float:

@@ -5,7 +5,7 @@
 set -u
 TAG=$1; WL=$2; KR=$3; CNT=$4
 mkdir -p gpurun_out
-CMD="python bench.py --workload $WL --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --streams 0"
+CMD="python bench.py --workload $WL --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --serial"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -5 gpurun_out/plain_$TAG.log; exit 1; }
 ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:"$KR" -c $CNT \
     -o gpurun_out/$TAG $CMD > gpurun_out/ncu_$TAG.log 2>&1
