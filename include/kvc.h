@@ -78,6 +78,12 @@ int kvc_plan_destroy(kvc_plan* plan);
 /* Canonical strategy id of the plan (NUL-terminated, owned by the plan). */
 const char* kvc_plan_strategy_id(const kvc_plan* plan);
 
+/* Kernel family kvc_encode / kvc_decode run for this plan: "fast128",
+ * "fast128+fixup", "uchan128", "fused_rc", "delta128", or "generic: <why>"
+ * (the per-element correctness kernels, e.g. float32 input).  Static strings. */
+const char* kvc_plan_encode_path(const kvc_plan* plan);
+const char* kvc_plan_decode_path(const kvc_plan* plan);
+
 int64_t kvc_metadata_bytes(const kvc_plan* plan);  /* exact metadata size          */
 int64_t kvc_payload_capacity(const kvc_plan* plan); /* upper bound on payload size   */
 int64_t kvc_workspace_bytes(const kvc_plan* plan);  /* scratch needed by encode/decode */

@@ -25,6 +25,8 @@ EXPORTS = (
     "kvc_plan_create",
     "kvc_plan_destroy",
     "kvc_plan_strategy_id",
+    "kvc_plan_encode_path",
+    "kvc_plan_decode_path",
     "kvc_metadata_bytes",
     "kvc_payload_capacity",
     "kvc_workspace_bytes",
@@ -45,6 +47,12 @@ EXPORTS = (
     "kvc_sq_error",
     "kvc_sq_error_partials",
 )
+
+
+class GenericKernelWarning(UserWarning):
+    """A plan runs the generic per-element CUDA kernels (still on the GPU, but
+    several times slower than the fused head_dim-128 kernels), e.g. for
+    float32 input that is not bf16-exact."""
 
 
 class CodecError(ValueError):
@@ -81,6 +89,9 @@ def lib() -> ctypes.CDLL:
     L.kvc_plan_destroy.restype = I32
     L.kvc_plan_strategy_id.argtypes = [P]
     L.kvc_plan_strategy_id.restype = ctypes.c_char_p
+    for name in ("kvc_plan_encode_path", "kvc_plan_decode_path"):
+        getattr(L, name).argtypes = [P]
+        getattr(L, name).restype = ctypes.c_char_p
     for name in ("kvc_metadata_bytes", "kvc_payload_capacity", "kvc_workspace_bytes", "kvc_max_blocks"):
         getattr(L, name).argtypes = [P]
         getattr(L, name).restype = I64

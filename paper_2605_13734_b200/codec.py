@@ -12,6 +12,7 @@ data-dependent codecs and ``KVCodec.check``.
 from __future__ import annotations
 
 import ctypes
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -87,6 +88,16 @@ class DeviceBlob:
         return self.offsets[: self.nblocks + 1].cpu().numpy().astype(np.int64)
 
 
+_WARNED: set = set()
+
+
+def _warn_generic(sid: str, side: str, path: str) -> None:
+    key = (sid, side, path)
+    if key not in _WARNED:
+        _WARNED.add(key)
+        warnings.warn(f"{sid}: {side} runs the {path}", N.GenericKernelWarning, stacklevel=3)
+
+
 class KVCodec:
     """A compiled plan (kvc_plan) plus its device workspace."""
 
@@ -120,6 +131,11 @@ class KVCodec:
         self._h = handle
         self._lib = lib
         self.strategy_id = lib.kvc_plan_strategy_id(handle).decode()
+        self.encode_path = lib.kvc_plan_encode_path(handle).decode()
+        self.decode_path = lib.kvc_plan_decode_path(handle).decode()
+        for side, path in (("encode", self.encode_path), ("decode", self.decode_path)):
+            if path.startswith("generic") and C == 128:
+                _warn_generic(self.strategy_id, side, path)
         self.metadata_bytes = int(lib.kvc_metadata_bytes(handle))
         self.payload_capacity = int(lib.kvc_payload_capacity(handle))
         self.max_blocks = int(lib.kvc_max_blocks(handle))

@@ -222,6 +222,9 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   g.block = (opt && opt->block_symbols) ? opt->block_symbols : 2048;
   if (g.block <= 0 || g.block % 8) return fail(KVC_ERR_CONFIG, "block_symbols must be a positive multiple of 8");
   g.uchan = g.quant == Q_UCHAN;
+  // a block that covers every symbol: rle codes the concatenated width
+  // streams as one block, byte for byte the reference's whole-tensor payload
+  g.rle_whole = g.codec == C_RLE && g.block >= g.E && g.E * 8 < (1ll << 31);
   g.rowlen = g.uchan ? T : C;
   if (g.rowlen % g.group)
     return fail(KVC_ERR_CONFIG, "group_size " + std::to_string(g.group) + " does not divide " +
@@ -307,6 +310,39 @@ int kvc_plan_destroy(kvc_plan* plan) {
 }
 
 const char* kvc_plan_strategy_id(const kvc_plan* plan) { return plan ? plan->p.id : ""; }
+
+// The kernel family kvc_encode / kvc_decode dispatch to for this plan (the
+// same predicates as the dispatch below), so callers can see -- and the
+// Python layer warns about -- a plan that runs the generic correctness
+// kernels instead of a fused head_dim-128 path.
+const char* kvc_plan_encode_path(const kvc_plan* plan) {
+  if (!plan) return "";
+  const Geo& g = plan->p.g;
+  if (fused_rc_applicable(g)) return "fused_rc";
+  if (fast128_applicable(g)) {
+    if (g.in_dtype != KVC_DTYPE_BF16) return "generic: float32 input (the fused kernels read bf16)";
+    if (2 * g.LH * g.T >= (1ll << 31)) return "generic: 2^30 or more token rows";
+    return g.transform == T_HADAMARD ? "fast128+fixup" : "fast128";
+  }
+  if (uchan128_applicable(g)) {
+    if (g.in_dtype != KVC_DTYPE_BF16) return "generic: float32 input (the fused kernels read bf16)";
+    if (g.LH * g.T >= (1ll << 31)) return "generic: 2^31 or more token rows";
+    return "uchan128";
+  }
+  if (g.C != 128) return "generic: head_dim is not 128";
+  return "generic: no fused kernel for this group / layout";
+}
+
+const char* kvc_plan_decode_path(const kvc_plan* plan) {
+  if (!plan) return "";
+  const Geo& g = plan->p.g;
+  if (fused_rc_applicable(g)) return "fused_rc";
+  if (delta128_applicable(g)) return "delta128";
+  if (fast128_applicable(g)) return "fast128";
+  if (uchan128_applicable(g)) return "uchan128";
+  if (g.C != 128) return "generic: head_dim is not 128";
+  return "generic: no fused kernel for this group / layout";
+}
 int64_t kvc_metadata_bytes(const kvc_plan* plan) { return plan ? plan->p.meta_bytes : -1; }
 int64_t kvc_payload_capacity(const kvc_plan* plan) { return plan ? plan->p.payload_cap : -1; }
 int64_t kvc_workspace_bytes(const kvc_plan* plan) { return plan ? plan->p.ws_bytes : -1; }
@@ -328,6 +364,7 @@ int64_t kvc_num_blocks(const kvc_plan* plan, const uint8_t* head_classes) {
   int n, w[2];
   int64_t cnt[2];
   host_streams(plan->p.g, head_classes, &n, w, cnt);
+  if (plan->p.g.rle_whole) return plan->p.g.E > 0 ? 1 : 0;
   int64_t b = 0;
   for (int i = 0; i < n; ++i) b += (cnt[i] + plan->p.g.block - 1) / plan->p.g.block;
   return b;

@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(128) k_rle_encode(CodecArgs a) {
     a.sizes[b] = 0;
     return;
   }
+  if (a.g.rle_whole) {  // the concatenated byte-padded streams (codecs.py:358-360)
+    rle_encode_block(a.packed_in, (int)st.packed_bytes, a.slots, a.slot_bytes, a.sizes, a.status);
+    return;
+  }
   const int si = block_stream(st, b);
   const int w = st.w[si];
   const int64_t start = (b - st.first_block[si]) * a.g.block;
@@ -157,9 +161,10 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
   if (b >= st.nblocks) return;
   const int si = block_stream(st, b);
   const int w = st.w[si];
-  const int64_t start = (b - st.first_block[si]) * a.g.block;
+  const int64_t start = a.g.rle_whole ? 0 : (b - st.first_block[si]) * a.g.block;
   const int64_t n = min(a.g.block, st.count[si] - start);
-  const int64_t want = (n * w + 7) / 8;
+  // whole-tensor rle: the block decodes to all packed streams, back to back
+  const int64_t want = a.g.rle_whole ? st.packed_bytes : (n * w + 7) / 8;
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
   // PackBits grows a block by at most one control byte per 128 literals
   if (o1 < o0 || o1 - o0 > (uint64_t)(want + want / 64 + 16) ||
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
   }
   const uint8_t* in = a.payload_in + o0;
   const int len = (int)(o1 - o0);
-  uint8_t* out = a.packed_out + st.byte_off[si] + start * w / 8;
+  uint8_t* out = a.packed_out + (a.g.rle_whole ? 0 : st.byte_off[si] + start * w / 8);
   // input: aligned words, clamped to the word holding the block's last byte
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uint32_t* iw = reinterpret_cast<const uint32_t*>(ia & ~(uintptr_t)3);

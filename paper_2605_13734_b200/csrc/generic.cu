@@ -53,6 +53,10 @@ __global__ void k_setup(Geo g, const uint8_t* meta, StreamTab* st, HeadEntry* he
         t.w[i] = 0; t.count[i] = 0; t.byte_off[i] = off; t.first_block[i] = blk;
       }
     }
+    if (g.rle_whole) {  // one rle block over all streams (the reference's whole-tensor format)
+      for (int i = 0; i < kMaxStreams; ++i) t.first_block[i] = 0;
+      blk = off > 0 ? 1 : 0;
+    }
     t.nblocks = blk;
     t.packed_bytes = off;
     *st = t;

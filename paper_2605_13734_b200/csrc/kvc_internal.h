@@ -31,6 +31,8 @@ struct Geo {
   int64_t meta_affine_off;  // byte offset of mu16||a16 in metadata (or -1)
   int64_t block;     // codec block in symbols
   int in_dtype, out_dtype;
+  int rle_whole;     // rle with one block covering the whole tensor: the block is
+                     // the concatenated packed width streams (codecs.py:358-360)
 };
 
 // Width streams (codecs.py:339-345): widths descending.

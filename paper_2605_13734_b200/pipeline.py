@@ -366,8 +366,18 @@ def _bits_per_head(s: StrategyConfig, shape, classes) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 
-def compress(x, s, timer: StageTimer | None = None, block_symbols: int = 2048):
-    """Encode + decode on the GPU and measure both sides (compress.py:111-140)."""
+def reference_block_symbols(shape) -> int:
+    """A codec block covering the whole tensor: rle / entropy payloads then
+    take the reference's whole-tensor format byte for byte (codecs.py:355-367;
+    one range-coded stream per width, rle over the concatenated streams), so
+    `cr` is the reference's own.  Decoding is then serial per width stream."""
+    E = int(np.prod(shape))
+    return max(8, (E + 7) // 8 * 8)
+
+
+def compress(x, s, timer: StageTimer | None = None, block_symbols: int | None = 2048):
+    """Encode + decode on the GPU and measure both sides (compress.py:111-140).
+    block_symbols=None: the reference's whole-tensor payload format."""
     s = as_strategy(s)
     if not isinstance(x, KVTensor):
         vals = x if isinstance(x, (torch.Tensor, np.ndarray)) else x.values
@@ -380,6 +390,8 @@ def compress(x, s, timer: StageTimer | None = None, block_symbols: int = 2048):
     if v.dtype not in (torch.bfloat16, torch.float32):
         v = v.float()
     nbytes = x.nbytes_source
+    if block_symbols is None:
+        block_symbols = reference_block_symbols(v.shape)
     codec = _plan(s.id, v.shape, v.dtype, block_symbols)
     classes = _classes_for(s, x)
     dblob, enc_s = timer.measure(lambda: codec.encode(v, head_classes=classes), nbytes, "encode", s)
@@ -446,9 +458,12 @@ def _checked_offsets(offsets, payload_len: int, nblocks: int) -> np.ndarray:
     return np.ascontiguousarray(o)
 
 
-def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_symbols: int = 2048):
-    """Full inverse pipeline on the GPU; returns (KVTensor fp32 on device, s_dec)."""
+def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_symbols: int | None = 2048):
+    """Full inverse pipeline on the GPU; returns (KVTensor fp32 on device, s_dec).
+    block_symbols=None: the blob is in the reference's whole-tensor format."""
     s = as_strategy(s)
+    if block_symbols is None:
+        block_symbols = reference_block_symbols(blob.shape)
     timer = timer if timer is not None else CudaEventTimer()
     _check_blob_matches(blob, s)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -498,7 +513,12 @@ class GpuCorpusEvaluator:
     then stores GPU s_enc/s_dec in each Profile (cli.py:111-121).
     """
 
-    def __init__(self, corpus, sample_size: int = 8, v_ref: float = float(2**30), timer=None, seed: int = 0) -> None:
+    def __init__(self, corpus, sample_size: int = 8, v_ref: float = float(2**30), timer=None, seed: int = 0,
+                 reference_format: bool = False) -> None:
+        """reference_format=True codes rle / entropy profiles in the reference's
+        whole-tensor payload format (one block per tensor), so `cr` equals the
+        reference CorpusEvaluator's; the default block-framed format (2048-symbol
+        blocks, parallel decode) costs ~1% of cr at 2 bits."""
         if sample_size < 1:
             raise ValueError("sample_size must be >= 1")
         if len(corpus) < sample_size:
@@ -508,7 +528,9 @@ class GpuCorpusEvaluator:
         self.v_ref = v_ref
         self.timer = timer if timer is not None else CudaEventTimer()
         self.seed = seed
+        self.reference_format = reference_format
         self.throughputs: dict[str, tuple[float, float]] = {}
+        self.picks: dict[str, list[int]] = {}
         self._dev: dict[int, KVTensor] = {}
 
     def _device_tensor(self, i: int) -> KVTensor:
@@ -525,11 +547,13 @@ class GpuCorpusEvaluator:
         sid = getattr(strategy, "id", s.id)
         rng = np.random.default_rng([self.seed, _stable_hash(sid)])
         picks = rng.choice(len(self.corpus), size=self.sample_size, replace=False)
+        self.picks[sid] = [int(i) for i in picks]
         total = enc = dec = 0.0
         accs, crs = [], []
+        block = None if self.reference_format else 2048
         for i in picks:
             x = self._device_tensor(int(i))
-            _, m = compress(x, s, self.timer)
+            _, m = compress(x, s, self.timer, block_symbols=block)
             accs.append(m.quality)
             crs.append(m.cr)
             total += x.nbytes_source

@@ -91,3 +91,45 @@ def test_canonical_rho_repr(lib):
     rc, h = _plan(lib, "t=delta;q=mixed,hi=4,lo=3,g=64,rho=0.1250;c=rle", shape=(1, 1, 4, 64))
     assert rc == 0
     assert lib.kvc_plan_strategy_id(h).decode() == "t=delta;q=mixed,hi=4,lo=3,g=64,rho=0.125;c=rle"
+
+
+def _plan_dtype(lib, sid, in_dtype, shape=(2, 4, 64, 128), block=2048):
+    h = ctypes.c_void_p()
+    o = N.KvcOptions()
+    o.block_symbols = block
+    o.in_dtype = in_dtype
+    assert lib.kvc_plan_create(ctypes.byref(h), sid.encode(), *shape, ctypes.byref(o)) == N.KVC_OK
+    return h
+
+
+@pytest.mark.parametrize("sid,bf16_path", [
+    ("t=hadamard;q=uniform,b=4,g=32;c=none", "fast128+fixup"),
+    ("t=identity;q=uniform,b=2,g=32;c=entropy", "fused_rc"),
+    ("t=identity;q=uchan,b=2,g=32;c=entropy", "fused_rc"),
+    ("t=identity;q=uchan,b=2,g=32;c=none", "uchan128"),
+    ("t=delta;q=uniform,b=4,g=16;c=none", "generic: no fused kernel for this group / layout"),
+])
+def test_plan_reports_its_kernel_path(lib, sid, bf16_path):
+    """kvc_plan_encode_path names the kernel family (the generic fallbacks
+    are visible, and KVCodec warns about them)."""
+    shape = (1, 2, 2048, 128)  # per-channel groups tile 128 tokens, fused blocks 2048
+    h = _plan_dtype(lib, sid, N.DTYPE_BF16, shape)
+    assert lib.kvc_plan_encode_path(h).decode() == bf16_path
+    lib.kvc_plan_destroy(h)
+    h = _plan_dtype(lib, sid, N.DTYPE_F32, shape)
+    assert lib.kvc_plan_encode_path(h).decode().startswith("generic")
+    lib.kvc_plan_destroy(h)
+
+
+def test_rle_block_covering_the_tensor_is_one_block(lib):
+    """block_symbols >= L*H*T*C with rle: one block over the concatenated
+    width streams (the reference's whole-tensor rle, codecs.py:358-360)."""
+    shape = (2, 4, 64, 128)
+    E = 2 * 4 * 64 * 128
+    h = _plan_dtype(lib, "t=identity;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=rle", N.DTYPE_BF16, shape, block=E)
+    cls = (ctypes.c_uint8 * 8)(1, 0, 0, 1, 0, 0, 0, 0)
+    assert lib.kvc_num_blocks(h, cls) == 1
+    lib.kvc_plan_destroy(h)
+    h = _plan_dtype(lib, "t=identity;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=rle", N.DTYPE_BF16, shape, block=E // 2)
+    assert lib.kvc_num_blocks(h, cls) > 1
+    lib.kvc_plan_destroy(h)
