@@ -531,9 +531,11 @@ def run_workload(workload: str, args, steps: int, rank: int, world: int, dev, do
 
 def measure_e2e(tensors, paged, steps, world, dev, V_all) -> dict:
     """Same metric end to end through the public API (hostpath.HostRoundTrip):
-    pinned host KV -> H2D -> encode -> wire into pinned host memory -> H2D ->
-    decode (contiguous or paged) -> D2H of the step's scalar result, pipelined
-    by layer chunks across copy engines, PCIe and SMs."""
+    pinned host KV -> H2D -> encode -> decode (contiguous or paged) -> D2H of
+    the step's scalar result, pipelined by layer chunks across copy engines,
+    PCIe and SMs; the blob stays in HBM as in the reference's compress().
+    "wire_via_host" repeats it with the compressed wire shipped to pinned host
+    memory and back between encode and decode (a network hop's PCIe cost)."""
     import torch
     import torch.distributed as dist
 
@@ -547,8 +549,34 @@ def measure_e2e(tensors, paged, steps, world, dev, V_all) -> dict:
     L_rank = tensors[0]["kv"].shape[0]
     chunk = max(1, min(8, L_rank // 4)) if L_rank >= 4 else L_rank
     pg = None if paged is None else (paged["table"], paged["page_tokens"], paged["layer_stride"])
-    rts = [HostRoundTrip(t["sid"], tuple(t["kv"].shape), chunk_layers=chunk, block_symbols=BLOCK, device=dev, paged=pg)
-           for t in tensors]
+    out = {}
+    for via_host in (False, True):
+        rts = [HostRoundTrip(t["sid"], tuple(t["kv"].shape), chunk_layers=chunk, block_symbols=BLOCK, device=dev,
+                             paged=pg, wire_via_host=via_host) for t in tensors]
+        ms = _time_e2e(rts, host_in, tensors, steps, world, dev)
+        wire = sum(rt.wire_bytes() for rt in rts)
+        h2d = sum(h.numel() * 2 for h in host_in) + (wire if via_host else 0)
+        d2h = (wire if via_host else 0) + 8
+        res_kind = "squared reconstruction error (fp64 scalar)" if paged is None else "compressed bytes (paged decode)"
+        path = ("pinned host KV -> H2D -> encode -> wire to pinned host -> H2D -> decode" if via_host else
+                "pinned host KV -> H2D -> encode -> decode (blob stays in HBM, as in compress())")
+        r = {"value": round(V_all / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": max(1, min(3, steps)),
+             "chunk_layers": chunk,
+             "path": f"{path} -> D2H of the {res_kind} (hostpath.HostRoundTrip, layer-chunk pipeline)"}
+        if via_host:
+            out["wire_via_host"] = r
+        else:
+            out.update(r)
+        del rts
+    del host_in
+    return out
+
+
+def _time_e2e(rts, host_in, tensors, steps, world, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
     result = torch.zeros((), dtype=torch.float64, device=dev)
 
     def e2e_step():
@@ -573,20 +601,11 @@ def measure_e2e(tensors, paged, steps, world, dev, V_all) -> dict:
     s1.record()
     torch.cuda.synchronize()
     ms = s0.elapsed_time(s1) / n
-    wire = sum(rt.wire_bytes() for rt in rts)
-    h2d = sum(h.numel() * 2 for h in host_in) + wire
-    d2h = wire + 8
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    res_kind = "squared reconstruction error (fp64 scalar)" if paged is None else "compressed bytes (paged decode)"
-    out = {"value": round(V_all / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": n, "chunk_layers": chunk,
-           "path": f"pinned host KV -> H2D -> encode -> wire to pinned host -> H2D -> decode -> D2H of the {res_kind} "
-                   "(hostpath.HostRoundTrip, layer-chunk pipeline)"}
-    del rts, host_in
-    return out
+    return ms
 
 
 def main():

@@ -33,14 +33,17 @@ __all__ = ["HostRoundTrip"]
 
 class HostRoundTrip:
     def __init__(self, strategy_id: str, shape, chunk_layers: int = 4, block_symbols: int = 2048, device=None,
-                 paged=None) -> None:
+                 paged=None, wire_via_host: bool = True) -> None:
         """paged = (block_table int32 cuda, page_tokens, layer_stride): decode
         into a paged cache (kvc_decode_paged; one table shared by every
         layer, `out` the page pool of all layers) instead of a contiguous
-        (L, H, T, C) tensor."""
+        (L, H, T, C) tensor.  wire_via_host=False: the blob stays in HBM
+        between encode and decode, as in the reference's compress()
+        (compress.py:122-130) -- only the KV crosses PCIe."""
         L, H, T, C = (int(v) for v in shape)
         self.shape = (L, H, T, C)
         self.paged = paged
+        self.wire_via_host = wire_via_host
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.chunks = [(l0, min(L, l0 + chunk_layers)) for l0 in range(0, L, chunk_layers)]
         enc_plans: dict[int, KVCodec] = {}
@@ -57,7 +60,9 @@ class HostRoundTrip:
                 self.enc.append(e)
                 self.dec.append(d)
                 self.blob.append(e.alloc_blob())
-                self.rx.append(d.alloc_blob())
+                self.rx.append(d.alloc_blob() if wire_via_host else self.blob[-1])
+                if not wire_via_host:
+                    continue
                 # the full payload capacity: the device-length copy can never
                 # truncate a chunk (a shorter buffer would drop bytes silently)
                 self.h_pay.append(torch.empty(max(e.payload_capacity, 16), dtype=torch.uint8, pin_memory=True))
@@ -95,11 +100,15 @@ class HostRoundTrip:
                 with torch.cuda.stream(self.s_in):
                     dev_in[l0:l1].copy_(host_kv[l0:l1], non_blocking=True)
                 self.e_in[i].record(self.s_in)
-                # encode (after the previous run's D2H read this chunk's blob)
+                # encode (after the previous run's D2H -- or decode -- read this chunk's blob)
                 self.s_enc.wait_event(self.e_in[i])
-                self.s_enc.wait_event(self.e_out[i])
+                self.s_enc.wait_event(self.e_out[i] if self.wire_via_host else self.e_dec[i])
                 enc.encode(dev_in[l0:l1], out=blob, stream=self.s_enc)
                 self.e_enc[i].record(self.s_enc)
+                if not self.wire_via_host:
+                    self.s_dec.wait_event(self.e_enc[i])
+                    self._decode(i, rx, blob, dec, out, dev_in, err_sum, device_length=blob.offsets is not None)
+                    continue
                 # wire -> pinned host (after the previous run's H2D of the wire)
                 self.s_out.wait_event(self.e_enc[i])
                 self.s_out.wait_event(self.e_back[i])
@@ -131,25 +140,30 @@ class HostRoundTrip:
                     self._copy(rx.payload.data_ptr(), hp.data_ptr(), big, blob.payload_nbytes(), self.s_back)
                 self.e_back[i].record(self.s_back)
                 rx.nblocks, rx._nbytes = blob.nblocks, blob._nbytes
-                # decode + error
                 self.s_dec.wait_event(self.e_back[i])
-                if self.paged is not None:
-                    table, page_tokens, stride = self.paged
-                    dec.decode_paged(rx, out[l0 * stride:l1 * stride], table, page_tokens, stride, stream=self.s_dec,
-                                     device_length=ho is not None)
-                    if err_sum is not None and ho is not None:  # the step's scalar: compressed bytes
-                        with torch.cuda.stream(self.s_dec):
-                            err_sum.add_(rx.offsets[rx.nblocks].to(torch.float64))
-                else:
-                    dec.decode(rx, out=out[l0:l1], stream=self.s_dec, device_length=ho is not None)
-                if err_sum is not None and self.paged is None:
-                    n = (l1 - l0) * self.shape[1] * self.shape[2] * self.shape[3]
-                    dt = N.DTYPE_BF16 if out.dtype == torch.bfloat16 else N.DTYPE_F32
-                    N.check(lib.kvc_sq_error(out[l0:l1].data_ptr(), dev_in[l0:l1].data_ptr(), n, dt,
-                                             err_sum.data_ptr(), _stream_handle(self.s_dec)))
-                self.e_dec[i].record(self.s_dec)
+                self._decode(i, rx, blob, dec, out, dev_in, err_sum, device_length=ho is not None)
             cur.wait_stream(self.s_dec)
         return err_sum
+
+    def _decode(self, i, rx, blob, dec, out, dev_in, err_sum, device_length: bool) -> None:
+        """Decode chunk i on s_dec and add the step's scalar result: the squared
+        reconstruction error (contiguous) or the compressed bytes (paged)."""
+        l0, l1 = self.chunks[i]
+        if self.paged is not None:
+            table, page_tokens, stride = self.paged
+            dec.decode_paged(rx, out[l0 * stride:l1 * stride], table, page_tokens, stride, stream=self.s_dec,
+                             device_length=device_length)
+            if err_sum is not None and rx.offsets is not None:
+                with torch.cuda.stream(self.s_dec):
+                    err_sum.add_(rx.offsets[rx.nblocks].to(torch.float64))
+        else:
+            dec.decode(rx, out=out[l0:l1], stream=self.s_dec, device_length=device_length)
+            if err_sum is not None:
+                n = (l1 - l0) * self.shape[1] * self.shape[2] * self.shape[3]
+                dt = N.DTYPE_BF16 if out.dtype == torch.bfloat16 else N.DTYPE_F32
+                N.check(N.lib().kvc_sq_error(out[l0:l1].data_ptr(), dev_in[l0:l1].data_ptr(), n, dt,
+                                             err_sum.data_ptr(), _stream_handle(self.s_dec)))
+        self.e_dec[i].record(self.s_dec)
 
     def check(self) -> None:
         for c in {id(c): c for c in self.enc}.values():
@@ -158,5 +172,6 @@ class HostRoundTrip:
             c.check(stream=self.s_dec, decoding=True)
 
     def wire_bytes(self) -> int:
+        """Compressed bytes of the last run (payload + metadata + block table)."""
         return sum(b.payload_nbytes() + b.metadata.numel() + (0 if b.offsets is None else 8 * (b.nblocks + 1))
                    for b in self.blob)
