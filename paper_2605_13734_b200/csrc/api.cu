@@ -276,7 +276,7 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
   // fused Hadamard encode: list of rows for the exact fixup pass (one int32
   // per token row at most, plus the count)
   p.ws_fix = -1;
-  if (g.transform == T_HADAMARD && fast128_applicable(g) && g.in_dtype == KVC_DTYPE_BF16) {
+  if (g.transform == T_HADAMARD && fast128_applicable(g)) {
     p.ws_fix = off;
     off = align_up(off + 16 + 4 * g.LH * g.T, 256);
   }
@@ -320,12 +320,12 @@ const char* kvc_plan_encode_path(const kvc_plan* plan) {
   const Geo& g = plan->p.g;
   if (fused_rc_applicable(g)) return "fused_rc";
   if (fast128_applicable(g)) {
-    if (g.in_dtype != KVC_DTYPE_BF16) return "generic: float32 input (the fused kernels read bf16)";
-    if (2 * g.LH * g.T >= (1ll << 31)) return "generic: 2^30 or more token rows";
+    const int64_t box_rows = (g.in_dtype == KVC_DTYPE_F32 ? 4 : 2) * g.LH * g.T;
+    if (box_rows >= (1ll << 31)) return "generic: too many token rows for a 2-D tensor map";
     return g.transform == T_HADAMARD ? "fast128+fixup" : "fast128";
   }
   if (uchan128_applicable(g)) {
-    if (g.in_dtype != KVC_DTYPE_BF16) return "generic: float32 input (the fused kernels read bf16)";
+    if (g.in_dtype != KVC_DTYPE_BF16) return "generic: float32 input (the per-channel kernels read bf16)";
     if (g.LH * g.T >= (1ll << 31)) return "generic: 2^31 or more token rows";
     return "uchan128";
   }
@@ -461,7 +461,7 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
   else
     e = launch_encode_generic(a, s);
   if (e != cudaSuccess) return cuda_fail(e, "encode kernel");
-  if (fix && fast128_applicable(g) && g.in_dtype == KVC_DTYPE_BF16 && g.LH * g.T < (1ll << 31)) {
+  if (fix && fast128_applicable(g) && g.LH * g.T < (1ll << 31)) {
     if ((e = launch_encode_fixup(a, s)) != cudaSuccess) return cuda_fail(e, "encode fixup");
   }
   if (g.codec != C_NONE) {

@@ -310,29 +310,49 @@ __device__ __forceinline__ void quantize64(float* y, float mn0, float mx0, float
 
 // ------------------------------------------------------------ encode kernel
 // W = compile-time symbol width (uniform strategies), 0 = per-row runtime width
-template <int MODE, int G, int W>
+// F32: float32 input (the reference's own corpora): the tile is 64 rows x
+// 512 B read as 128-byte quarter rows (2 stages of 32 KB keep 3 CTAs/SM), and
+// every mode reads each value's float32 bit pattern instead of unpacking bf16.
+template <bool F32>
+__host__ __device__ constexpr int enc_stages() {
+  return F32 ? 2 : kStages;
+}
+template <bool F32>
+__host__ __device__ constexpr int enc_tile_bytes() {
+  return F32 ? 2 * kTileBytes : kTileBytes;
+}
+template <bool F32>
+__host__ __device__ constexpr int enc_smem_bytes() {
+  return enc_stages<F32>() * enc_tile_bytes<F32>() + 1024 + 64;
+}
+
+template <int MODE, int G, int W, bool F32 = false>
 __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
+  constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + kStages * kTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + NS * TB);
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows;
   const int tid = threadIdx.x, half = tid & 1;
   const uint32_t sw = (uint32_t)(tid & 7);
 
+  // tensor-map coordinate of a tile: 128-byte box rows (bf16 half rows,
+  // fp32 quarter rows)
+  constexpr int kBoxRows = F32 ? 4 * kRows : 2 * kRows;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < ntiles) {
-        mbar_expect_tx(&full[s], kTileBytes);
-        tma_load_2d(tiles + s * kTileBytes, &tmap, 0, (int)(tile * kThreads), &full[s]);
+        mbar_expect_tx(&full[s], TB);
+        tma_load_2d(tiles + s * TB, &tmap, 0, (int)(tile * kBoxRows), &full[s]);
       }
     }
   }
@@ -341,33 +361,46 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
   uint32_t flags = 0;
   float nanacc = 0.0f;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int s = it % kStages;
-    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
-    const uint8_t* tb = tiles + s * kTileBytes;
-    uint32_t wv[32];
+  // this thread's values from a tile row (swizzled 128-byte box rows); w[]
+  // holds 32 bf16 pairs or 64 fp32 bit patterns
+  auto load_half = [&](const uint8_t* tb, int r, uint32_t* w) {
+    constexpr int kBoxPer = F32 ? 2 : 1;  // 128-byte box rows per half row
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint4 c = *reinterpret_cast<const uint4*>(tb + tid * 128 + (((uint32_t)k ^ sw) << 4));
-      wv[4 * k] = c.x; wv[4 * k + 1] = c.y; wv[4 * k + 2] = c.z; wv[4 * k + 3] = c.w;
+    for (int q = 0; q < kBoxPer; ++q) {
+      const int br = kBoxPer * r + q;
+      const uint32_t bsw = (uint32_t)(br & 7);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint4 c = *reinterpret_cast<const uint4*>(tb + br * 128 + (((uint32_t)k ^ bsw) << 4));
+        w[32 * q + 4 * k] = c.x; w[32 * q + 4 * k + 1] = c.y; w[32 * q + 4 * k + 2] = c.z; w[32 * q + 4 * k + 3] = c.w;
+      }
     }
+  };
+  constexpr int NW = F32 ? 64 : 32;
+  // float32 bit pattern of local value i
+  auto vbits = [&](const uint32_t* w, int i) -> uint32_t {
+    if constexpr (F32) return w[i];
+    return (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
+  };
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % NS;
+    mbar_wait(&full[s], (uint32_t)((it / NS) & 1));
+    const uint8_t* tb = tiles + s * TB;
+    uint32_t wv[NW];
+    load_half(tb, tid, wv);
     const int64_t row = tile * kRows + (tid >> 1);
     const bool valid = row < nrows;
     const int64_t lh = valid ? row / g.T : 0;
     const int64_t t = valid ? row - lh * g.T : 0;
-    uint32_t pv[32];  // delta: previous row's half
+    uint32_t pv[NW];  // delta: previous row's half
     if (MODE == M_DELTA) {
       if (tid >= 2) {
-        const uint32_t psw = (uint32_t)((tid - 2) & 7);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          uint4 c = *reinterpret_cast<const uint4*>(tb + (tid - 2) * 128 + (((uint32_t)k ^ psw) << 4));
-          pv[4 * k] = c.x; pv[4 * k + 1] = c.y; pv[4 * k + 2] = c.z; pv[4 * k + 3] = c.w;
-        }
+        load_half(tb, tid - 2, pv);
       } else if (valid && t > 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + (row - 1) * 128 + half * 64);
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) +
+                                                          ((row - 1) * 128 + half * 64) * (F32 ? 4 : 2));
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < NW / 4; ++k) {
           uint4 c = __ldg(src + k);
           pv[4 * k] = c.x; pv[4 * k + 1] = c.y; pv[4 * k + 2] = c.z; pv[4 * k + 3] = c.w;
         }
@@ -375,11 +408,11 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     }
     __syncthreads();  // every thread has its half-row in registers: slot s is free
     if (tid == 0) {
-      const int64_t next = tile + (int64_t)kStages * gridDim.x;
+      const int64_t next = tile + (int64_t)NS * gridDim.x;
       if (next < ntiles) {
         fence_proxy_async();
-        mbar_expect_tx(&full[s], kTileBytes);
-        tma_load_2d(tiles + s * kTileBytes, &tmap, 0, (int)(next * kThreads), &full[s]);
+        mbar_expect_tx(&full[s], TB);
+        tma_load_2d(tiles + s * TB, &tmap, 0, (int)(next * kBoxRows), &full[s]);
       }
     }
     // invalid tail rows run the same code (shuffles need the full warp) but
@@ -399,7 +432,20 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       // (tensors.py:41-42).  Zeros, extreme magnitudes and near-midpoint
       // results send the row to the exact fixup pass (k_encode_fixup).
       bool row_ok;
-      {
+      if constexpr (F32) {  // |x| as unsigned bit patterns order like the floats
+        uint32_t amx = wv[0] & 0x7FFFFFFFu, amn = amx;
+#pragma unroll
+        for (int k = 1; k < 64; ++k) {
+          const uint32_t aw = wv[k] & 0x7FFFFFFFu;
+          amx = max(amx, aw);
+          amn = min(amn, aw);
+        }
+        if (amx >= 0x7F800000u) nanacc = 1.0f;
+        amx = max(amx, (uint32_t)__shfl_xor_sync(0xffffffffu, amx, 1));
+        amn = min(amn, (uint32_t)__shfl_xor_sync(0xffffffffu, amn, 1));
+        const uint32_t emax = (amx >> 23) & 0xFFu, emin = (amn >> 23) & 0xFFu;
+        row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+      } else {
         uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
 #pragma unroll
         for (int k = 1; k < 32; ++k) {
@@ -417,10 +463,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       }
       double f[64];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        f[2 * j] = f32bits_scaled_f64(wv[j] << 16);
-        f[2 * j + 1] = f32bits_scaled_f64(wv[j] & 0xFFFF0000u);
-      }
+      for (int i = 0; i < 64; ++i) f[i] = f32bits_scaled_f64(vbits(wv, i));
       // stages h = 1..32 (transforms.py:41-46 order), in registers.  At h = 32
       // thread B (half 1) writes its two outputs swapped (u - v at i, u + v at
       // i + 32; the same roundings, as one DFMA with -1 each), so afterwards
@@ -479,16 +522,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       hadlayout = true;
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        y[2 * j] = __uint_as_float(wv[j] << 16);
-        y[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
-      }
+      for (int i = 0; i < 64; ++i) y[i] = __uint_as_float(vbits(wv, i));
       if (MODE == M_DELTA && t > 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          y[2 * j] = __fsub_rn(y[2 * j], __uint_as_float(pv[j] << 16));
-          y[2 * j + 1] = __fsub_rn(y[2 * j + 1], __uint_as_float(pv[j] & 0xFFFF0000u));
-        }
+        for (int i = 0; i < 64; ++i) y[i] = __fsub_rn(y[i], __uint_as_float(vbits(pv, i)));
       }
       if (MODE == M_AFFINE) {
         const uint4* mu = reinterpret_cast<const uint4*>(a.meta + g.meta_affine_off + (lh * 128 + half * 64) * 2);
@@ -518,11 +555,18 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       cb1 = 64 * half + 32;
     }
     float mn0, mx0, mn1, mx1;
-    if (MODE == M_IDENTITY) {
+    if (MODE == M_IDENTITY && !F32) {
       // exact bf16 min/max, two per instruction; NaN / inf surface here
       minmax32_bf16(wv, mn0, mx0);
       minmax32_bf16(wv + 16, mn1, mx1);
       if (!(isfinite(mn0) && isfinite(mx0) && isfinite(mn1) && isfinite(mx1))) nanacc = 1.0f;
+    } else if (MODE == M_IDENTITY) {
+      minmax32(y, mn0, mx0);
+      minmax32(y + 32, mn1, mx1);
+      uint32_t amx = 0;  // fminf / fmaxf drop NaNs: test the bit patterns
+#pragma unroll
+      for (int i = 0; i < 64; ++i) amx = max(amx, wv[i] & 0x7FFFFFFFu);
+      if (amx >= 0x7F800000u) nanacc = 1.0f;
     } else {
       minmax32(y, mn0, mx0);
       minmax32(y + 32, mn1, mx1);
@@ -951,37 +995,62 @@ bool make_input_map(CUtensorMap* map, const void* kv, int64_t nrows, int box_row
   return r == CUDA_SUCCESS;
 }
 
-template <int MODE, int G, int W>
+// the (rows, 128) fp32 tensor viewed as (4*rows, 32): one 128 B quarter row per box row
+bool make_input_map_f32(CUtensorMap* map, const void* kv, int64_t nrows) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {32, (cuuint64_t)(4 * nrows)};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {32, (cuuint32_t)(4 * kRows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(kv), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
-  auto k = k_enc128<MODE, G, W>;
-  set_max_dyn_smem<k_enc128<MODE, G, W>>(kSmemBytes);
+  constexpr int smem = enc_smem_bytes<F32>();
+  auto k = k_enc128<MODE, G, W, F32>;
+  set_max_dyn_smem<k_enc128<MODE, G, W, F32>>(smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t ntiles = (a.g.LH * a.g.T + kRows - 1) / kRows;
   int64_t grid = (int64_t)sm_count * per_sm;
   if (grid > ntiles) grid = ntiles;
-  k<<<(unsigned)grid, kThreads, kSmemBytes, s>>>(map, a);
+  k<<<(unsigned)grid, kThreads, smem, s>>>(map, a);
   return cudaGetLastError();
 }
 
-template <int MODE, int G>
+template <int MODE, int G, bool F32>
 cudaError_t launch_enc_w(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   const int w = a.g.quant == Q_UNIFORM ? a.g.bits : 0;
   switch (w) {
-    case 2: return launch_enc<MODE, G, 2>(map, a, sm_count, s);
-    case 4: return launch_enc<MODE, G, 4>(map, a, sm_count, s);
-    case 8: return launch_enc<MODE, G, 8>(map, a, sm_count, s);
-    default: return launch_enc<MODE, G, 0>(map, a, sm_count, s);
+    case 2: return launch_enc<MODE, G, 2, F32>(map, a, sm_count, s);
+    case 4: return launch_enc<MODE, G, 4, F32>(map, a, sm_count, s);
+    case 8: return launch_enc<MODE, G, 8, F32>(map, a, sm_count, s);
+    default: return launch_enc<MODE, G, 0, F32>(map, a, sm_count, s);
   }
 }
 
-template <int MODE>
+template <int MODE, bool F32>
 cudaError_t launch_enc_g(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   switch (a.g.group) {
-    case 32: return launch_enc_w<MODE, 32>(map, a, sm_count, s);
-    case 64: return launch_enc_w<MODE, 64>(map, a, sm_count, s);
-    default: return launch_enc_w<MODE, 128>(map, a, sm_count, s);
+    case 32: return launch_enc_w<MODE, 32, F32>(map, a, sm_count, s);
+    case 64: return launch_enc_w<MODE, 64, F32>(map, a, sm_count, s);
+    default: return launch_enc_w<MODE, 128, F32>(map, a, sm_count, s);
+  }
+}
+
+template <bool F32>
+cudaError_t launch_enc_t(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
+  switch (a.g.transform) {
+    case T_IDENTITY: return launch_enc_g<M_IDENTITY, F32>(map, a, sm_count, s);
+    case T_DELTA: return launch_enc_g<M_DELTA, F32>(map, a, sm_count, s);
+    case T_HADAMARD: return launch_enc_g<M_HADAMARD, F32>(map, a, sm_count, s);
+    default: return launch_enc_g<M_AFFINE, F32>(map, a, sm_count, s);
   }
 }
 
@@ -1089,18 +1158,14 @@ bool fast128_applicable(const Geo& g) {
 }
 
 cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s) {
-  if (a.g.in_dtype != KVC_DTYPE_BF16) return launch_encode_generic(a, s);
+  const bool f32 = a.g.in_dtype == KVC_DTYPE_F32;
   const int64_t nrows = a.g.LH * a.g.T;
-  if (2 * nrows >= (1ll << 31)) return launch_encode_generic(a, s);
+  if ((f32 ? 4 : 2) * nrows >= (1ll << 31)) return launch_encode_generic(a, s);
   CUtensorMap map;
-  if (!make_input_map(&map, a.kv, nrows)) return launch_encode_generic(a, s);
+  if (!(f32 ? make_input_map_f32(&map, a.kv, nrows) : make_input_map(&map, a.kv, nrows)))
+    return launch_encode_generic(a, s);
   ProfScope ps("encode_fast128", s);
-  switch (a.g.transform) {
-    case T_IDENTITY: return launch_enc_g<M_IDENTITY>(map, a, sm_count, s);
-    case T_DELTA: return launch_enc_g<M_DELTA>(map, a, sm_count, s);
-    case T_HADAMARD: return launch_enc_g<M_HADAMARD>(map, a, sm_count, s);
-    default: return launch_enc_g<M_AFFINE>(map, a, sm_count, s);
-  }
+  return f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
 }
 
 cudaError_t launch_decode_fast128(const DecArgs& a, int sm_count, cudaStream_t s) {

@@ -102,14 +102,14 @@ def _plan_dtype(lib, sid, in_dtype, shape=(2, 4, 64, 128), block=2048):
     return h
 
 
-@pytest.mark.parametrize("sid,bf16_path", [
-    ("t=hadamard;q=uniform,b=4,g=32;c=none", "fast128+fixup"),
-    ("t=identity;q=uniform,b=2,g=32;c=entropy", "fused_rc"),
-    ("t=identity;q=uchan,b=2,g=32;c=entropy", "fused_rc"),
-    ("t=identity;q=uchan,b=2,g=32;c=none", "uchan128"),
-    ("t=delta;q=uniform,b=4,g=16;c=none", "generic: no fused kernel for this group / layout"),
+@pytest.mark.parametrize("sid,bf16_path,f32_path", [
+    ("t=hadamard;q=uniform,b=4,g=32;c=none", "fast128+fixup", "fast128+fixup"),
+    ("t=identity;q=uniform,b=2,g=32;c=entropy", "fused_rc", "fast128"),
+    ("t=identity;q=uchan,b=2,g=32;c=entropy", "fused_rc", "generic"),
+    ("t=identity;q=uchan,b=2,g=32;c=none", "uchan128", "generic"),
+    ("t=delta;q=uniform,b=4,g=16;c=none", "generic: no fused kernel for this group / layout", "generic"),
 ])
-def test_plan_reports_its_kernel_path(lib, sid, bf16_path):
+def test_plan_reports_its_kernel_path(lib, sid, bf16_path, f32_path):
     """kvc_plan_encode_path names the kernel family (the generic fallbacks
     are visible, and KVCodec warns about them)."""
     shape = (1, 2, 2048, 128)  # per-channel groups tile 128 tokens, fused blocks 2048
@@ -117,7 +117,7 @@ def test_plan_reports_its_kernel_path(lib, sid, bf16_path):
     assert lib.kvc_plan_encode_path(h).decode() == bf16_path
     lib.kvc_plan_destroy(h)
     h = _plan_dtype(lib, sid, N.DTYPE_F32, shape)
-    assert lib.kvc_plan_encode_path(h).decode().startswith("generic")
+    assert lib.kvc_plan_encode_path(h).decode().startswith(f32_path)
     lib.kvc_plan_destroy(h)
 
 

@@ -476,3 +476,40 @@ def test_staged_bf16_decode_matches_fp32_decode(sid, shape):
     ref = oracle.encode_blob(vb, None, sid)
     rec = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, shape)
     assert_decoded(o32.cpu().numpy(), rec, sid, shape)
+
+
+@pytest.mark.parametrize("t", ["identity", "delta", "hadamard", "affine"])
+@pytest.mark.parametrize("g", [32, 64, 128])
+@pytest.mark.parametrize("b", [2, 3, 4, 8])
+def test_f32_fast_path_matches_oracle(t, g, b):
+    """float32 inputs that are NOT bf16-exact (the reference's own corpora,
+    tensors.py:102-103) take the fused head_dim-128 encoder (fp32 tensor tiles,
+    2-stage ring): payload, scales and zeros bit-exact against the oracle,
+    including a partial last tile (104 rows)."""
+    from paper_2605_13734_b200 import KVCodec
+
+    sid = f"t={t};q=uniform,b={b},g={g};c=none"
+    shape = (1, 1, 104, 128) if t != "delta" else (2, 1, 104, 128)  # 104 rows: a partial tile
+    v, imp = oracle.generate_kv(*shape, seed=17 * b + g)
+    codec = KVCodec(sid, shape, in_dtype=torch.float32, out_dtype=torch.float32)
+    assert codec.encode_path.startswith("fast128"), codec.encode_path
+    blob = codec.encode(torch.from_numpy(v).cuda())
+    codec.check()
+    ref = oracle.encode_blob(v, imp, sid)
+    assert blob.metadata_bytes() == ref["metadata"], sid
+    assert blob.payload_bytes() == ref["payload"], sid
+
+
+def test_f32_fast_path_flags_nonfinite():
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (1, 2, 64, 128)
+    v, _ = oracle.generate_kv(*shape, seed=2)
+    for sid in ("t=identity;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=4,g=32;c=none"):
+        for bad in (np.nan, np.inf):
+            x = v.copy()
+            x[0, 1, 33, 77] = bad
+            codec = KVCodec(sid, shape, in_dtype=torch.float32)
+            codec.encode(torch.from_numpy(x).cuda())
+            with pytest.raises(ValueError):
+                codec.check()
