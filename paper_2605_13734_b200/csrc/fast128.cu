@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
 template <int MODE, int G>
 __device__ __forceinline__ bool dec_core(float* y, const float* sc, const float* zr, int half, int64_t lh,
                                          const DecArgs& a, const float* aff_rc = nullptr,
-                                         const float* aff_mu = nullptr) {
+                                         const float* aff_mu = nullptr, const float* aff_a = nullptr) {
   static_assert(G >= 32, "fast path groups");
   const Geo& g = a.g;
   bool groups_finite = true;
@@ -675,23 +675,27 @@ __device__ __forceinline__ bool dec_core(float* y, const float* sc, const float*
       Y[16 + i] = f2mul(Y[16 + i], c1);
     }
   } else if (MODE == M_AFFINE) {
-    if (aff_rc) {  // the tile's per-channel RN(1/a) and mu from shared memory
+    // x = y / a + mu with the division correctly rounded (div_by_rcp)
+    if (aff_rc) {  // the tile's per-channel a, RN(1/a) and mu from shared memory
       const float4* rc4 = reinterpret_cast<const float4*>(aff_rc + half * 64);
       const float4* mu4 = reinterpret_cast<const float4*>(aff_mu + half * 64);
+      const float4* a4 = reinterpret_cast<const float4*>(aff_a + half * 64);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const float4 r = rc4[k], m = mu4[k];
-        y[4 * k] = __fadd_rn(__fmul_rn(y[4 * k], r.x), m.x);
-        y[4 * k + 1] = __fadd_rn(__fmul_rn(y[4 * k + 1], r.y), m.y);
-        y[4 * k + 2] = __fadd_rn(__fmul_rn(y[4 * k + 2], r.z), m.z);
-        y[4 * k + 3] = __fadd_rn(__fmul_rn(y[4 * k + 3], r.w), m.w);
+        const float4 r = rc4[k], m = mu4[k], av = a4[k];
+        y[4 * k] = __fadd_rn(div_by_rcp(y[4 * k], av.x, r.x), m.x);
+        y[4 * k + 1] = __fadd_rn(div_by_rcp(y[4 * k + 1], av.y, r.y), m.y);
+        y[4 * k + 2] = __fadd_rn(div_by_rcp(y[4 * k + 2], av.z, r.z), m.z);
+        y[4 * k + 3] = __fadd_rn(div_by_rcp(y[4 * k + 3], av.w, r.w), m.w);
       }
     } else {
       const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off) + lh * 128 + half * 64;
       const __half* scl = mu + g.LH * 128;
 #pragma unroll
-      for (int i = 0; i < 64; ++i)
-        y[i] = __fadd_rn(__fmul_rn(y[i], __frcp_rn(__half2float(scl[i]))), __half2float(mu[i]));
+      for (int i = 0; i < 64; ++i) {
+        const float av = __half2float(scl[i]);
+        y[i] = __fadd_rn(div_by_rcp(y[i], av, __frcp_rn(av)), __half2float(mu[i]));
+      }
     }
   }
   return groups_finite;
@@ -825,7 +829,7 @@ __host__ __device__ constexpr int dec_stage_bytes() {
 }
 template <int MODE, int W, int G>
 __host__ __device__ constexpr int dec_smem_bytes() {
-  return 2 * kTileBytes + dec_stages<W>() * dec_stage_bytes<MODE, W, G>() + 1024 + 64 + (MODE == M_AFFINE ? 4 * 128 * 4 : 0);
+  return 2 * kTileBytes + dec_stages<W>() * dec_stage_bytes<MODE, W, G>() + 1024 + 64 + (MODE == M_AFFINE ? 6 * 128 * 4 : 0);
 }
 
 template <int MODE, int G, int W, bool PAGED>
@@ -915,11 +919,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
       const int64_t t0 = tile * kRows - (tile * kRows / g.T) * g.T + 16 * warp;
       page_id = a.block_table[(t0 + (int64_t)lane * bt) / a.page_tokens];
     }
-    float* arc = aff_tab + (it & 1) * 256;
+    float* arc = aff_tab + (it & 1) * 384;
     float* amu = arc + 128;
+    float* aav = arc + 256;
     if (tabs) {  // the tile's per-channel tables from the stage (every tile of the ring is full)
       const __half* mu = reinterpret_cast<const __half*>(ibuf + s * STAGE + PK + 2 * SB);
-      arc[tid] = __frcp_rn(__half2float(mu[128 + tid]));
+      const float av = __half2float(mu[128 + tid]);
+      arc[tid] = __frcp_rn(av);
+      aav[tid] = av;
       amu[tid] = __half2float(mu[tid]);
     }
     // contiguous output: one tensor store per tile from obuf[it & 1], whose
@@ -934,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
       }
     }
     const bool groups_finite =
-        dec_core<MODE, G>(y, sc, zr, half, lh, a, tabs ? arc : nullptr, tabs ? amu : nullptr);
+        dec_core<MODE, G>(y, sc, zr, half, lh, a, tabs ? arc : nullptr, tabs ? amu : nullptr, tabs ? aav : nullptr);
     if (valid) dec_flags<MODE>(y, groups_finite, flags);
     // paged: this warp's buffer of two tiles ago must have been read out
     if (PAGED && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");

@@ -162,6 +162,16 @@ __device__ __forceinline__ uint32_t quant_one(float v, const GroupQ& q) {
   return quant_slow(v, q.z, q.s, q.lv);
 }
 
+// y / a correctly rounded (the oracle's affine inverse divides)
+// from r = RN(1/a): q0 = RN(y r), the exact residual y - a q0 by one FMA, and
+// one correction step RN(q0 + r (y - a q0)) (Markstein: r correctly rounded
+// and q0 within an ulp give the correctly rounded quotient; a is an fp16
+// value, so no intermediate over/underflows for finite decoded y).
+__device__ __forceinline__ float div_by_rcp(float y, float a, float r) {
+  const float q0 = __fmul_rn(y, r);
+  return __fmaf_rn(__fmaf_rn(-q0, a, y), r, q0);
+}
+
 // dequantize (quantize.py:178): zero + symbol*scale, unfused.
 __device__ __forceinline__ float dequant(uint32_t sym, float s, float z) {
   return __fadd_rn(z, __fmul_rn(__uint_as_float(0x4B000000u | sym) - 8388608.0f, s));

@@ -257,16 +257,17 @@ __global__ void __launch_bounds__(kUThreads, 3) k_dec_uchan128(const DecArgs a) 
       for (int k = 0; k < W; ++k) wd[k] = stage_sym[(c * 4 + warp) * W + k];
       unpack32_words<W>(wd, outv[j]);
       const float s = stage_sz[(c * 4 + warp) * 2], z = stage_sz[(c * 4 + warp) * 2 + 1];
-      float m = 0.0f, rs = 1.0f;
+      float m = 0.0f, av = 1.0f, rs = 1.0f;
       if (AFFINE) {
         const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off);
         m = __half2float(mu[lh * 128 + c]);
-        rs = __frcp_rn(__half2float(mu[g.LH * 128 + lh * 128 + c]));
+        av = __half2float(mu[g.LH * 128 + lh * 128 + c]);
+        rs = __frcp_rn(av);
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         float x = __fadd_rn(z, __fmul_rn(outv[j][i], s));
-        if (AFFINE) x = __fadd_rn(__fmul_rn(x, rs), m);
+        if (AFFINE) x = __fadd_rn(div_by_rcp(x, av, rs), m);  // y / a correctly rounded
         outv[j][i] = x;
       }
     }

@@ -81,12 +81,13 @@ def fast_path(sid, shape, in_f32=False):
 
 def assert_decoded(got, rec, sid, shape, in_f32=False):
     """Decoded values: bit-exact where the kernel reproduces the reference's
-    arithmetic; the fused head_dim-128 decode runs the inverse Hadamard in fp32
-    and the inverse affine as a reciprocal multiply, so those are held to the
+    arithmetic (identity, delta, and the affine inverse, whose division is
+    correctly rounded from the reciprocal by one residual step); the fused
+    head_dim-128 decode runs the inverse Hadamard in fp32, held to the
     reference's own transform tolerance (1e-5, test_acceptance.py:235) scaled
     by the row magnitude."""
     t = oracle.parse_id(sid).transform
-    if fast_path(sid, shape, in_f32) and t in ("hadamard", "affine"):
+    if fast_path(sid, shape, in_f32) and t == "hadamard":
         rowmax = np.abs(rec).max(axis=-1, keepdims=True)
         assert np.all(np.abs(got - rec) <= 1e-5 * rowmax + 1e-30), (sid, float(np.abs(got - rec).max()))
     else:
@@ -513,3 +514,39 @@ def test_f32_fast_path_flags_nonfinite():
             codec.encode(torch.from_numpy(x).cuda())
             with pytest.raises(ValueError):
                 codec.check()
+
+
+@pytest.mark.parametrize("sid", ["t=affine;q=uniform,b=8,g=32;c=none", "t=affine;q=uniform,b=4,g=64;c=none",
+                                 "t=affine;q=uchan,b=4,g=32;c=none", "t=affine;q=uniform,b=8,g=32;c=entropy"])
+@pytest.mark.parametrize("out", ["f32", "bf16"])
+def test_affine_decode_is_the_oracle_division(sid, out):
+    """The affine inverse y / a + mu (oracle/extensions.py affine_inv) with a
+    correctly rounded division: per-channel scales spread over 2^-12 .. 2^12
+    so a takes thousands of fp16 values; fp32 output bit-exact, bf16 output
+    equal to bf16(oracle) -- contiguous, and for bf16 also paged."""
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (2, 8, 256, 128)
+    rng = np.random.default_rng(99)
+    v = (rng.standard_normal(shape) * np.exp2(rng.uniform(-12, 12, size=shape[:2] + (1, shape[3])))).astype(np.float32)
+    tb, vb = bf16_exact(v)
+    ref = oracle.encode_blob(vb, None, sid, block=2048)
+    rec = oracle.decode_blob(ref["payload"], ref["metadata"], ref["offsets"], sid, shape, block=2048)
+    dt = torch.float32 if out == "f32" else torch.bfloat16
+    codec = KVCodec(sid, shape, out_dtype=dt)
+    blob = codec.encode(tb.cuda())
+    codec.check()
+    assert blob.payload_bytes() == ref["payload"]
+    got = codec.decode(blob)
+    codec.check(decoding=True)
+    want = torch.from_numpy(rec).to(dt)
+    assert torch.equal(got.cpu().view(torch.int16 if out == "bf16" else torch.int32),
+                       want.view(torch.int16 if out == "bf16" else torch.int32)), sid
+    if out == "bf16":
+        L, H, T, C = shape
+        pt, n_pages = 16, T // 16
+        table = torch.randperm(n_pages, device="cuda").to(torch.int32)
+        pool = torch.empty(L * n_pages * pt * H * C, dtype=torch.bfloat16, device="cuda")
+        codec.decode_paged(blob, pool, table, pt, n_pages * pt * H * C)
+        view = pool.view(L, n_pages, pt, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
+        assert torch.equal(view.cpu(), want), sid
