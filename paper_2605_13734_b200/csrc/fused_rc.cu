@@ -230,7 +230,9 @@ __device__ __forceinline__ void store_rows(const uint8_t* tile, Tout* dst, int l
     const int rr = k * kRowsPer + lane / kPer, ch = lane % kPer;
     const uint64_t p = __shfl_sync(0xffffffffu, mine, rr);
     const bool ok = __shfl_sync(0xffffffffu, live, rr);
-    if (ok) reinterpret_cast<uint4*>(p)[ch] = *reinterpret_cast<const uint4*>(tile + rr * kStride + 16 * ch);
+    // streaming stores (evict-first): the decoded KV is written once and must not
+    // push the coded blocks, still being read, out of L2
+    if (ok) __stcs(reinterpret_cast<uint4*>(p) + ch, *reinterpret_cast<const uint4*>(tile + rr * kStride + 16 * ch));
   }
 }
 
@@ -260,7 +262,7 @@ __device__ __forceinline__ void tok_encode_groups(const FusedArgs& a, const uint
     uint32_t wv[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint4 v = __ldg(src + gi * 4 + k);
+      const uint4 v = __ldcs(src + gi * 4 + k);  // read once: evict-first, keeps the coded slots in L2
       wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
     }
     if (gi + 1 < ngr) {  // next group's 64 bytes
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
     const uint4* rowp = src + (int64_t)gi * 32 * 16;  // 32 tokens = 32 * 256 B
     uint4 v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = __ldg(rowp + k);
+    for (int k = 0; k < 4; ++k) v[k] = __ldcs(rowp + k);  // read once (evict-first)
     if (gi + 1 < ngr) {
       prefetch_l1(rowp + 32 * 16);
       prefetch_l1(rowp + 32 * 16 + 2);
