@@ -19,8 +19,11 @@ largest single-GPU config, is the headline):
   c2  Llama-3.1-8B 32K  (32,8,32768,128)  K: t=identity;q=uchan,b=2,g=32;c=entropy (KIVI per-channel)
                                            V: t=identity;q=uniform,b=2,g=32;c=entropy (per-token)
   c5  Qwen3-8B 16K      (36,8,16384,128)  K,V: t=affine;q=uniform,b=8,g=32;c=entropy, decoded into paged KV
-At N=1 the default run also measures c1, c2 and c5 and nests them under
-"extra" (same fields, fewer steps).  Multi-GPU: torchrun, one process per
+  c4  Llama-3.1-8B 16K   (32,8,16384,128)  the mixed-precision profiles (per-layer mixlayer,
+                                           per-token mixtok, per-head mixed; 36 ids), swept
+At N=1 the default run also measures c1, c2, c4 and c5 and nests them under
+"extra" (same fields, fewer steps; c4 as an aggregate + per-profile list).
+Multi-GPU: torchrun, one process per
 GPU; no collective on the data path -- only the per-rank compressed sizes
 are all-gathered (offsets for the wire).
 
@@ -59,7 +62,21 @@ WORKLOADS = {
                tensors=[("K", "t=affine;q=uniform,b=8,g=32;c=entropy"), ("V", "t=affine;q=uniform,b=8,g=32;c=entropy")],
                shard=False, paged=True),
 }
-EXTRAS = ("c1", "c2", "c5")
+EXTRAS = ("c1", "c2", "c4", "c5")
+# BASELINE configs[3]: the mixed-precision profiles of the strategy space --
+# per-layer (q=mixlayer) and per-token (q=mixtok) mixed precision, plus the
+# reference's per-head mixed_head -- on Llama-3.1-8B KV at 16K tokens
+C4_SHAPE = (32, 8, 16384, 128)
+
+
+def c4_ids() -> list[str]:
+    ids = []
+    for t in ("identity", "hadamard"):
+        for kind in ("mixlayer", "mixtok", "mixed"):
+            for hi, lo in ((8, 2), (4, 2), (8, 4)):
+                for c in ("none", "entropy"):
+                    ids.append(f"t={t};q={kind},hi={hi},lo={lo},g=32,rho=0.25;c={c}")
+    return ids
 EXTRA_STEPS = 5
 BLOCK = 2048
 PAGE_TOKENS = 16
@@ -529,6 +546,82 @@ def run_workload(workload: str, args, steps: int, rank: int, world: int, dev, do
     return res
 
 
+def run_sweep(args, steps: int, rank: int, world: int, dev, hbm_peak: float) -> dict:
+    """c4: the round trip of every mixed-precision profile (K and V, one
+    stream each) on the same synthetic 8B 16K cache; value = all profiles'
+    bf16-in bytes / their summed step time (per-profile numbers alongside)."""
+    import torch
+
+    from paper_2605_13734_b200 import KVCodec
+    from paper_2605_13734_b200 import _native as N
+    from paper_2605_13734_b200.pipeline import classify_heads, layer_classes
+    from paper_2605_13734_b200.synth import synthetic_kv
+
+    L, H, T, C = C4_SHAPE
+    E = L * H * T * C
+    kvs = []
+    for ti in range(2):
+        kv, imp = synthetic_kv(L, H, T, C, seed=4000 + 1000 * rank + ti, device=dev)
+        kvs.append((kv, imp, torch.empty_like(kv)))
+    main = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream(device=dev) for _ in kvs]
+    rows, tot_bytes, tot_ms = [], 0, 0.0
+    for sid in c4_ids():
+        codecs, blobs, cls = [], [], []
+        for kv, imp, _ in kvs:
+            c = KVCodec(sid, C4_SHAPE, block_symbols=BLOCK, device=dev)
+            q = sid.split(";")[1]
+            k = classify_heads(imp, 0.25) if q.startswith("q=mixed") else (
+                layer_classes(imp, 0.25) if q.startswith("q=mixlayer") else None)
+            codecs.append(c)
+            cls.append(k)
+            blobs.append(c.alloc_blob(k))
+
+        def step():
+            e = torch.cuda.Event()
+            e.record(main)
+            for st, c, (kv, _, out), b, k in zip(streams, codecs, kvs, blobs, cls):
+                st.wait_event(e)
+                c.encode(kv, head_classes=k, out=b, stream=st)
+                c.decode(b, out=out, device_length=True, stream=st)
+            for st in streams:
+                f = torch.cuda.Event()
+                f.record(st)
+                main.wait_event(f)
+
+        step()
+        for c in codecs:
+            c.check(decoding=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        comp = sum(b.compressed_nbytes for b in blobs)
+        qual = []
+        for (kv, _, out) in kvs:
+            se = torch.zeros((), dtype=torch.float64, device=dev)
+            sx = torch.zeros((), dtype=torch.float64, device=dev)
+            N.check(N.lib().kvc_sq_error(kv.data_ptr(), out.data_ptr(), E, N.DTYPE_BF16, se.data_ptr(), None))
+            N.check(N.lib().kvc_sq_error(kv.data_ptr(), None, E, N.DTYPE_BF16, sx.data_ptr(), None))
+            rmse, rms = math.sqrt(float(se) / E), math.sqrt(float(sx) / E)
+            qual.append(max(0.0, 1.0 - rmse / rms) if rmse > 1e-9 else 1.0)
+        V = 2 * E * len(kvs)
+        rows.append({"id": sid, "gbs": round(V / (ms * 1e-3) / 1e9, 1), "cr": round(V / comp, 4),
+                     "quality": round(sum(qual) / len(qual), 6)})
+        tot_bytes += V
+        tot_ms += ms
+        del codecs, blobs
+    gbs = sorted(r["gbs"] for r in rows)
+    return {"value": round(tot_bytes / (tot_ms * 1e-3) / 1e9, 3), "unit": "GB/s", "steps": steps,
+            "ms_per_step": round(tot_ms, 4), "config": {"workload": "c4", "shape": list(C4_SHAPE),
+                                                        "profiles": len(rows), "rho": 0.25},
+            "median_profile_gbs": gbs[len(gbs) // 2], "min_profile_gbs": gbs[0], "max_profile_gbs": gbs[-1],
+            "profiles": rows}
+
+
 def measure_e2e(tensors, paged, steps, world, dev, V_all) -> dict:
     """Same metric end to end through the public API (hostpath.HostRoundTrip):
     pinned host KV -> H2D -> encode -> decode (contiguous or paged) -> D2H of
@@ -647,6 +740,9 @@ def main():
                         strip(cpus.get(args.workload)), hbm_peak, peak_src)
     extra = {}
     for w in extras:
+        if w == "c4":
+            extra[w] = run_sweep(args, 3, rank, world, dev, hbm_peak)
+            continue
         extra[w] = run_workload(w, args, EXTRA_STEPS, rank, world, dev, (w == "c5") and not args.no_e2e,
                                 strip(cpus.get(w)), hbm_peak, peak_src)
 
