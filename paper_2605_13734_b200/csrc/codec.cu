@@ -7,11 +7,9 @@
 // decoding is parallel (one thread per block):
 //   entropy block = BE32(len) || range_encode(block, 1 << w)  (codecs.py:245-270, :310-317, :364-366)
 //   rle block     = rle_encode(packed block bytes)             (codecs.py:112-152)
-// Encode writes each block into a worst-case-sized scratch slot, then an
-// exclusive scan of the sizes gives block_offsets and a gather kernel packs
-// the slots into the payload.
-#include <cub/device/device_scan.cuh>
-
+// Encode writes each block into a worst-case-sized scratch slot, then one
+// kernel (k_scan_offsets: single-pass decoupled look-back) turns the sizes into
+// block_offsets and k_gather packs the slots into the payload.
 #include "kernels.h"
 #include "profile.h"
 #include "rc_tables.cuh"
@@ -240,57 +238,112 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
 // head / tail words byte by byte (they are shared with the neighbouring
 // blocks), the aligned body as 32-bit words funnel-shifted out of the
 // 16-byte-aligned slot
-__global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * 8;
-  const StreamTab& st = *a.st;
-  const int64_t nb = st.nblocks;
-  // grid-stride over blocks; the next block's offsets are loaded while the
-  // current one is copied
-  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint64_t o0 = 0, o1 = 0;
-  if (b < nb) {
-    o0 = a.offsets[b];
-    o1 = a.offsets[b + 1];
+// one warp copies block b's bytes [o0, o1) of the payload from its slot: the
+// unaligned head / tail bytewise, the body as 32-bit words funnel-shifted out
+// of the 16-byte-aligned slot, U words per lane in flight
+__device__ __forceinline__ void copy_block(const CodecArgs& a, int64_t b, uint64_t o0, uint64_t o1, int lane) {
+  const uint32_t len = (uint32_t)(o1 - o0);
+  const uint8_t* src = a.slots + b * a.slot_bytes;
+  uint8_t* dst = a.payload_out + o0;
+  const uint32_t head = min((uint32_t)((4u - (uint32_t)(o0 & 3u)) & 3u), len);
+  const uint32_t words = (len - head) >> 2;
+  const uint32_t tail = len - head - 4 * words;
+  if (lane < (int)head) dst[lane] = src[lane];
+  if (lane < (int)tail) dst[head + 4 * words + lane] = src[head + 4 * words + lane];
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
+  const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
+  // all loads of a round before any store (slots and payload never overlap,
+  // but the compiler cannot know that and would serialize them)
+  constexpr uint32_t U = 4;
+  for (uint32_t w0 = lane; w0 < words; w0 += 32 * U) {
+    uint32_t lo[U], hi[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t w = w0 + 32 * u;
+      lo[u] = w < words ? __ldg(s32 + w) : 0u;
+      hi[u] = (w < words && sh) ? __ldg(s32 + w + 1) : 0u;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t w = w0 + 32 * u;
+      if (w < words) d32[w] = sh ? __funnelshift_r(lo[u], hi[u], sh) : lo[u];
+    }
   }
-  for (; b < nb; b += nwarps) {
-    const int64_t bn = b + nwarps;
-    uint64_t n0 = 0, n1 = 0;
-    if (bn < nb) {
-      n0 = a.offsets[bn];
-      n1 = a.offsets[bn + 1];
-    }
-    const uint32_t len = (uint32_t)(o1 - o0);
-    const uint8_t* src = a.slots + b * a.slot_bytes;
-    uint8_t* dst = a.payload_out + o0;
-    const uint32_t head = min((uint32_t)((4u - (uint32_t)(o0 & 3u)) & 3u), len);
-    const uint32_t words = (len - head) >> 2;
-    const uint32_t tail = len - head - 4 * words;
-    if (lane < (int)head) dst[lane] = src[lane];
-    if (lane < (int)tail) dst[head + 4 * words + lane] = src[head + 4 * words + lane];
-    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
-    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
-    const uint32_t sh = 8 * head;  // src byte offset of the body inside its first word
-    // U words per lane per round, all loads issued before any store (slots
-    // and payload never overlap, but the compiler cannot know that and would
-    // otherwise serialize each load behind the previous store)
-    constexpr uint32_t U = 4;
-    for (uint32_t w0 = lane; w0 < words; w0 += 32 * U) {
-      uint32_t lo[U], hi[U];
+}
+
+// Block offsets in one pass over the sizes (single-pass decoupled look-back,
+// no library scan): CTAs take tiles of kScanTile block sizes in launch order
+// (an atomic ticket, so every lower tile has started and will finish: the
+// look-back cannot deadlock), scan them in shared memory, publish the tile
+// aggregate, then thread 0 walks back over the predecessors' published
+// aggregates / inclusive prefixes until it meets an inclusive one.
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+constexpr uint64_t kStAgg = 1ull << 62, kStInc = 2ull << 62, kStVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_offsets(CodecArgs a, uint64_t* status, uint32_t* ticket) {
+  __shared__ uint64_t warp_sum[kScanThreads / 32];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t n = a.max_blocks + 1;  // sizes / offsets entries
+  const int64_t b0 = tile * kScanTile + (int64_t)tid * kScanItems;
+  // kScanItems consecutive sizes per thread, summed locally
+  uint64_t v[kScanItems], mine = 0;
 #pragma unroll
-      for (uint32_t u = 0; u < U; ++u) {
-        const uint32_t w = w0 + 32 * u;
-        lo[u] = w < words ? __ldg(s32 + w) : 0u;
-        hi[u] = (w < words && sh) ? __ldg(s32 + w + 1) : 0u;
-      }
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = b0 + k < n ? a.sizes[b0 + k] : 0ull;
+    mine += v[k];
+  }
+  uint64_t incl = mine;
 #pragma unroll
-      for (uint32_t u = 0; u < U; ++u) {
-        const uint32_t w = w0 + 32 * u;
-        if (w < words) d32[w] = sh ? __funnelshift_r(lo[u], hi[u], sh) : lo[u];
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sum[warp] = incl;
+  __syncthreads();
+  uint64_t wpre = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    if (w < warp) wpre += warp_sum[w];
+    agg += warp_sum[w];
+  }
+  if (tid == 0) {
+    uint64_t prefix = 0;
+    if (tile == 0) {
+      st_status(status + tile, kStInc | agg);
+    } else {
+      st_status(status + tile, kStAgg | agg);
+      for (int64_t t = tile - 1; t >= 0; --t) {
+        uint64_t st;
+        while (((st = ld_status(status + t)) & ~kStVal) == 0ull) {
+        }
+        prefix += st & kStVal;
+        if (st & kStInc) break;
       }
+      st_status(status + tile, kStInc | (prefix + agg));
     }
-    o0 = n0;
-    o1 = n1;
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  uint64_t off = s_prefix + wpre + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (b0 + k < n) a.offsets[b0 + k] = off;
+    off += v[k];
   }
 }
 
@@ -317,10 +370,35 @@ void widths_used(const Geo& g, bool used[9]) {
 
 }  // namespace
 
+// slots -> payload, one warp per block, grid-stride; the next block's offsets
+// are loaded while the current one is copied
+__global__ void __launch_bounds__(256) k_gather(CodecArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  const int64_t nb = a.st->nblocks;
+  int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint64_t o0 = 0, o1 = 0;
+  if (b < nb) {
+    o0 = a.offsets[b];
+    o1 = a.offsets[b + 1];
+  }
+  for (; b < nb; b += nwarps) {
+    const int64_t bn = b + nwarps;
+    uint64_t n0 = 0, n1 = 0;
+    if (bn < nb) {
+      n0 = a.offsets[bn];
+      n1 = a.offsets[bn + 1];
+    }
+    copy_block(a, b, o0, o1, lane);
+    o0 = n0;
+    o1 = n1;
+  }
+}
+
+// look-back state: a ticket counter, then one status word per tile
 size_t codec_scan_bytes(int64_t max_blocks) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)(max_blocks + 1));
-  return bytes + 256;
+  const int64_t tiles = (max_blocks + 1 + kScanTile - 1) / kScanTile;
+  return (size_t)(16 + 8 * tiles);
 }
 
 cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_t s) {
@@ -350,18 +428,21 @@ cudaError_t launch_codec_encode(const CodecArgs& args, int sm_count, cudaStream_
 }
 
 cudaError_t launch_codec_finish(const CodecArgs& a, cudaStream_t s) {
-  size_t tmp = a.scan_bytes;
-  cudaError_t e;
+  const int64_t tiles = (a.max_blocks + 1 + kScanTile - 1) / kScanTile;
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(a.scan_tmp);
+  uint64_t* status = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(a.scan_tmp) + 16);
+  cudaError_t e = cudaMemsetAsync(a.scan_tmp, 0, codec_scan_bytes(a.max_blocks), s);
+  if (e != cudaSuccess) return e;
   {
     ProfScope ps("offset_scan", s);
-    e = cub::DeviceScan::ExclusiveSum(a.scan_tmp, tmp, a.sizes, a.offsets, (int)(a.max_blocks + 1), s);
+    k_scan_offsets<<<(unsigned)tiles, kScanThreads, 0, s>>>(a, status, ticket);
   }
-  if (e != cudaSuccess) return e;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (a.max_blocks * 32 + 255) / 256 + 1;
-  const int64_t cap = (int64_t)sms * 16;  // 16 CTAs of 8 warps per SM, grid-stride beyond
+  const int64_t cap = (int64_t)sms * 16;
   const unsigned ggrid = (unsigned)(want < cap ? want : cap);
   ProfScope ps("gather", s);
   k_gather<<<ggrid, 256, 0, s>>>(a);
