@@ -29,7 +29,6 @@ constexpr int kThreads = 128;            // 64 rows per tile
 constexpr int kRows = kThreads / 2;
 constexpr int kStages = 3;
 constexpr int kTileBytes = kThreads * 128;  // one 128 B half-row per thread
-constexpr int kSmemBytes = kStages * kTileBytes + 1024 + 64;
 
 enum Mode { M_IDENTITY = 0, M_DELTA = 1, M_HADAMARD = 2, M_AFFINE = 3 };
 
@@ -337,7 +336,6 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows;
   const int tid = threadIdx.x, half = tid & 1;
-  const uint32_t sw = (uint32_t)(tid & 7);
 
   // tensor-map coordinate of a tile: 128-byte box rows (bf16 half rows,
   // fp32 quarter rows)
