@@ -550,3 +550,31 @@ def test_affine_decode_is_the_oracle_division(sid, out):
         codec.decode_paged(blob, pool, table, pt, n_pages * pt * H * C)
         view = pool.view(L, n_pages, pt, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
         assert torch.equal(view.cpu(), want), sid
+
+
+@pytest.mark.parametrize("sid", ["t=identity;q=uniform,b=4,g=32;c=none", "t=identity;q=uniform,b=2,g=32;c=entropy",
+                                 "t=identity;q=uchan,b=4,g=32;c=none"])
+def test_signed_zero_group_minimum(sid):
+    """A group whose minimum is a zero of one sign keeps that sign in its
+    fp16 zero (quantize.py:147): -0.0 -> 0x8000, +0.0 -> 0x0000, as the
+    reference gives (probed: zeros bits [32768, 0] for these rows).  Groups
+    whose minimum is BOTH +0 and -0 are left out: numpy's SIMD min returns
+    either sign depending on lane order."""
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (1, 2, 128, 128)
+    rng = np.random.default_rng(5)
+    v = (np.abs(rng.standard_normal(shape)) + 0.5).astype(np.float32)
+    v[0, 0, 0, 5] = -0.0   # per-token group 0 of row 0: min -0
+    v[0, 0, 1, 7] = 0.0    # row 1: min +0
+    v[0, 1, 3, 40] = -0.0  # per-channel group (channel 40, tokens 0..31): min -0
+    v[0, 1, 64, 41] = 0.0  # channel 41, tokens 64..95: min +0
+    tb, vb = bf16_exact(v)
+    ref = oracle.encode_blob(vb, None, sid, block=2048)
+    codec = KVCodec(sid, shape, out_dtype=torch.float32)
+    blob = codec.encode(tb.cuda())
+    codec.check()
+    assert blob.metadata_bytes() == ref["metadata"], sid
+    assert blob.payload_bytes() == ref["payload"], sid
+    zeros = np.frombuffer(ref["metadata"], dtype=np.uint16)[len(ref["metadata"]) // 4:]
+    assert (zeros == 0x8000).any() and (zeros == 0).any()
