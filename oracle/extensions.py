@@ -178,6 +178,13 @@ def blob_streams(sym_l: np.ndarray, bits: np.ndarray):
     return out
 
 
+def rle_whole(s, n_symbols: int, block: int) -> bool:
+    """A block covering every symbol frames rle as ONE block over the
+    concatenated byte-padded width streams: the reference's whole-tensor rle
+    payload (codecs.py:358-360), mixed widths included (api.cu Geo::rle_whole)."""
+    return s.codec == "rle" and block >= n_symbols and n_symbols * 8 < (1 << 31)
+
+
 def encode_blob(values, importance, sid: str, block: int = 4096):
     """Returns dict(payload, metadata, offsets, streams, symbols, scales, zeros, y).
 
@@ -207,6 +214,9 @@ def encode_blob(values, importance, sid: str, block: int = 4096):
     offsets = None
     if s.codec == "none":
         payload = b"".join(pack_bits(st, w) for w, st in streams)
+    elif rle_whole(s, v.size, block):
+        payload = rle_encode(b"".join(pack_bits(st, w) for w, st in streams))
+        offsets = np.array([0, len(payload)] if payload else [0], dtype=np.int64)
     else:
         if block <= 0 or block % 8:
             raise ValueError("block must be a positive multiple of 8")
@@ -275,12 +285,19 @@ def decode_blob(payload: bytes, metadata: bytes, offsets, sid: str, shape, block
     sym = np.zeros(lshape, dtype=np.uint8)
     off = 0
     blk = 0
+    whole = None
+    if rle_whole(s, L * H * T * C, block):
+        nbytes = sum((int((bits == w).sum()) * lshape[3] * w + 7) // 8 for w in {int(b) for b in bits.reshape(-1)})
+        seg = payload[offsets[0] : offsets[-1]] if offsets is not None and len(offsets) > 1 else b""
+        whole = rle_decode(seg, cap=nbytes + 130) if seg else b""
+        if len(whole) != nbytes:
+            raise OracleError("rle payload decodes to the wrong length")
     for w in sorted({int(b) for b in bits.reshape(-1)}, reverse=True):
         mask = bits == w
         count = int(mask.sum()) * lshape[3]
-        if s.codec == "none":
+        if s.codec == "none" or whole is not None:
             nbytes = (count * w + 7) // 8
-            st = unpack_bits(payload[off : off + nbytes], w, count)
+            st = unpack_bits((whole if whole is not None else payload)[off : off + nbytes], w, count)
             off += nbytes
         else:
             pieces = []
@@ -301,6 +318,8 @@ def decode_blob(payload: bytes, metadata: bytes, offsets, sid: str, shape, block
             st = np.concatenate(pieces) if pieces else np.zeros(0, dtype=np.uint8)
             off = int(offsets[blk]) if offsets is not None and len(offsets) else off
         sym[mask] = st.reshape(-1, lshape[3])
+    if whole is not None:
+        off = int(offsets[-1]) if offsets is not None and len(offsets) else 0
     if off != len(payload):
         raise OracleError(f"{len(payload) - off} trailing bytes in payload")
     deq = dequantize_rows(sym, scales, zeros, s.group)

@@ -102,8 +102,7 @@ template <typename Tin>
 __global__ void k_affine_calibrate(Geo g, const Tin* kv, uint8_t* meta) {
   const int64_t lh = blockIdx.x;
   const int64_t nt = g.T < kAffinePrefix ? g.T : kAffinePrefix;
-  __half* mu = reinterpret_cast<__half*>(meta + g.meta_affine_off);
-  __half* a = mu + g.LH * g.C;
+  uint8_t* aff = meta + g.meta_affine_off;  // mu16[LH*C] || a16[LH*C]
   for (int64_t c = threadIdx.x; c < g.C; c += blockDim.x) {
     float mx = -INFINITY, mn = INFINITY;
     for (int64_t t = 0; t < nt; ++t) {
@@ -115,8 +114,8 @@ __global__ void k_affine_calibrate(Geo g, const Tin* kv, uint8_t* meta) {
     float r = __fsub_rn(mx, mn);
     float s = r > 0.0f ? __fdiv_rn(2.0f, r) : 1.0f;
     s = fminf(s, 65504.0f);
-    mu[lh * g.C + c] = __float2half_rn(m);
-    a[lh * g.C + c] = __float2half_rn(s);
+    st_meta_half(aff, lh * g.C + c, m);
+    st_meta_half(aff, g.LH * g.C + lh * g.C + c, s);
   }
 }
 
@@ -208,11 +207,10 @@ __device__ void encode_tile(const EncArgs& a, int TT, int64_t lh, int64_t t0, in
       __syncwarp();
     }
   } else if (g.transform == T_AFFINE) {
-    const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off);
-    const __half* sc = mu + g.LH * C;
+    const uint8_t* aff = a.meta + g.meta_affine_off;
     for (int64_t i = threadIdx.x; i < (int64_t)nt * C; i += blockDim.x) {
       int64_t c = i % C;
-      float v = __fmul_rn(__fsub_rn(y[i], __half2float(mu[lh * C + c])), __half2float(sc[lh * C + c]));
+      float v = __fmul_rn(__fsub_rn(y[i], ld_meta_half(aff, lh * C + c)), ld_meta_half(aff, (g.LH + lh) * C + c));
       if (!isfinite(v)) flags |= KVC_FLAG_NONFINITE_TRANSFORM;
       y[i] = v;
     }
@@ -361,11 +359,10 @@ __global__ void __launch_bounds__(256) k_decode_generic(DecArgs a, int TT) {
     }
     __syncthreads();
   } else if (g.transform == T_AFFINE) {
-    const __half* mu = reinterpret_cast<const __half*>(a.meta + g.meta_affine_off);
-    const __half* sc = mu + g.LH * C;
+    const uint8_t* aff = a.meta + g.meta_affine_off;
     for (int64_t i = threadIdx.x; i < (int64_t)nt * C; i += blockDim.x) {
       int64_t c = i % C;
-      y[i] = __fadd_rn(__fdiv_rn(y[i], __half2float(sc[lh * C + c])), __half2float(mu[lh * C + c]));
+      y[i] = __fadd_rn(__fdiv_rn(y[i], ld_meta_half(aff, (g.LH + lh) * C + c)), ld_meta_half(aff, lh * C + c));
     }
     __syncthreads();
   }

@@ -34,6 +34,21 @@ __device__ __forceinline__ void store_f32<__nv_bfloat16>(__nv_bfloat16* p, int64
   p[i] = __float2bfloat16_rn(v);
 }
 
+// fp16 affine parameters sit right after the class bits in the metadata, so
+// their byte offset can be odd: the generic kernels move them a byte at a time
+__device__ __forceinline__ float ld_meta_half(const uint8_t* base, int64_t i) {
+  const uint8_t* q = base + 2 * i;
+  return __half2float(__ushort_as_half((unsigned short)(q[0] | (q[1] << 8))));
+}
+__device__ __forceinline__ void st_meta_half(uint8_t* base, int64_t i, float v) {
+  // the f16 bits are widened to 32 bits inside PTX: ptxas (12.9) turns a byte
+  // store of a 16-bit f16 register into a value conversion (F2I.U8.F16)
+  unsigned w;
+  asm("{\n\t.reg .b16 h;\n\tcvt.rn.f16.f32 h, %1;\n\tcvt.u32.u16 %0, h;\n\t}" : "=r"(w) : "f"(v));
+  base[2 * i] = (uint8_t)(w & 0xffu);
+  base[2 * i + 1] = (uint8_t)(w >> 8);
+}
+
 // ---------------------------------------------------------------------------
 // Hadamard (transforms.py:33-47, :62): fp64 butterfly, / RN64(sqrt n), -> f32.
 //

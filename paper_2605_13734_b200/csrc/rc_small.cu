@@ -64,7 +64,10 @@ __global__ void __launch_bounds__(128) k_rc_small_encode(CodecArgs a) {
   RcEnc e;
   e.init(reinterpret_cast<uint32_t*>(slot + 4));
   constexpr int GS = Grp<W>::kSyms, GW = Grp<W>::kWords;
-  const int n1 = min(n, kH) / GS;  // whole groups in the reciprocal-table phase
+  // whole groups in the reciprocal-table phase, read as words when the stream
+  // is word aligned (the second width stream of a mixed tensor need not be)
+  const bool aligned = (reinterpret_cast<uintptr_t>(src) & 3) == 0;
+  const int n1 = aligned ? min(n, kH) / GS : 0;
   for (int gI = 0; gI < n1; ++gI) {
     uint32_t wd[GW], mg[GS];
 #pragma unroll

@@ -220,6 +220,56 @@ def test_parity_all_180_ids_small(channels):
         assert_decoded(got, rec, sid, shape)
 
 
+@pytest.mark.parametrize("channels", [64, 128])
+def test_parity_all_180_ids_default_block(channels):
+    """Every strategy-space id at the reference's default 2048-symbol block,
+    on a multi-block tensor (512 coded blocks for b=8): bitstream, offsets and
+    metadata bit-exact, decode as assert_decoded."""
+    from kv_space import all_ids
+
+    shape = (2, 8, 512, channels)
+    for k, sid in enumerate(all_ids()):
+        got, rec, _ = run_case(sid, shape, seed=100 + k, block=2048)
+        assert_decoded(got, rec, sid, shape)
+
+
+def _fuzz_case(k):
+    """Seeded random (id, shape, block, in_f32) over the extended grammar:
+    every transform, quant kind, width 1..8, group and codec, with shapes the
+    oracle accepts (g | C; power-of-two C for hadamard; g | T for uchan)."""
+    rng = np.random.default_rng(9000 + k)
+    t = ["identity", "delta", "hadamard", "affine"][rng.integers(4)]
+    q = ["uniform", "uchan", "mixed", "mixtok", "mixlayer"][rng.integers(5)]
+    c = ["none", "rle", "entropy"][rng.integers(3)]
+    if t == "hadamard":
+        C = int(2 ** rng.integers(2, 9))
+    else:
+        C = int(rng.choice([4, 8, 12, 20, 32, 48, 64, 96, 128, 160, 256]))
+    gs = [g for g in (1, 2, 4, 8, 16, 32, 64, 128) if C % g == 0]
+    g = int(rng.choice(gs))
+    L, H = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+    T = int(rng.integers(1, 300))
+    if q == "uchan":
+        g = int(rng.choice([g for g in (1, 2, 4, 8, 16, 32, 64) if g <= 64]))
+        T = max(1, T // g) * g
+    if q in ("uniform", "uchan"):
+        qs = f"{q},b={int(rng.integers(1, 9))},g={g}"
+    else:
+        hi = int(rng.integers(2, 9))
+        lo = int(rng.integers(1, hi))
+        qs = f"{q},hi={hi},lo={lo},g={g},rho={float(rng.choice([0.0, 0.125, 0.3, 0.5, 1.0]))!r}"
+    block = int(rng.choice([16, 64, 128, 256, 2048]))
+    in_f32 = bool(rng.integers(4) == 0)
+    return f"t={t};q={qs};c={c}", (L, H, T, C), block, in_f32
+
+
+@pytest.mark.parametrize("k", range(200))
+def test_parity_fuzz(k):
+    sid, shape, block, in_f32 = _fuzz_case(k)
+    got, rec, _ = run_case(sid, shape, seed=k, block=block, in_f32=in_f32)
+    assert_decoded(got, rec, sid, shape, in_f32=in_f32)
+
+
 def test_f32_input_matches_reference_fixture():
     """fp32 (non-bf16) inputs: the golden whole-tensor blobs from the reference."""
     from golden_io import items, load

@@ -29,7 +29,9 @@ def test_golden_180_whole_tensor_blobs(g180):
         s = oracle.parse_id(sid)
         whole = oracle.pipeline.whole_payload(ob["streams"], s.codec)
         assert whole == pays[k], sid
-        if s.codec == "none":
+        if s.codec in ("none", "rle"):
+            # rle with a block covering the tensor is framed as ONE block over
+            # the concatenated width streams: the reference payload itself
             assert ob["payload"] == pays[k], sid
 
 
