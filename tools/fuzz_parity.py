@@ -2,7 +2,9 @@
 failure; a CUDA error poisons the context, so the process exits and the
 caller restarts it after the failing index.
 
-    python tools/fuzz_parity.py START END   -> prints 'FAIL k sid shape block f32 : msg' / 'DONE k'
+    python tools/fuzz_parity.py START END [fused]  -> prints 'FAIL k sid shape block f32 : msg' / 'DONE k'
+
+`fused` draws from _fuzz_case_fast (head_dim-128 shapes for the fused kernels).
 """
 import os
 import sys
@@ -18,8 +20,9 @@ import test_gpu_parity as T  # noqa: E402
 
 def main():
     a, b = int(sys.argv[1]), int(sys.argv[2])
+    gen = T._fuzz_case_fast if len(sys.argv) > 3 and sys.argv[3] == "fused" else T._fuzz_case
     for k in range(a, b):
-        sid, shape, block, f32 = T._fuzz_case(k)
+        sid, shape, block, f32 = gen(k)
         try:
             got, rec, _ = T.run_case(sid, shape, seed=k, block=block, in_f32=f32)
             T.assert_decoded(got, rec, sid, shape, in_f32=f32)
