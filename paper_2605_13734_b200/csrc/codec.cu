@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128) k_rle_decode(CodecArgs a) {
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
   // PackBits grows a block by at most one control byte per 128 literals
   if (o1 < o0 || o1 - o0 > (uint64_t)(want + want / 64 + 16) ||
-      (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
+      (a.payload_bytes >= 0 && o1 > (uint64_t)a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }
@@ -356,7 +356,7 @@ __global__ void k_check_payload(CodecArgs a) {
     return;
   }
   if (a.offsets_in[0] != 0) atomicOr(a.status, KVC_FLAG_CODEC);
-  if (a.payload_bytes >= 0 && (int64_t)a.offsets_in[st.nblocks] != a.payload_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
+  if (a.payload_bytes >= 0 && a.offsets_in[st.nblocks] != (uint64_t)a.payload_bytes) atomicOr(a.status, KVC_FLAG_CODEC);
 }
 
 void widths_used(const Geo& g, bool used[9]) {

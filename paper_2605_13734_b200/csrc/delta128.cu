@@ -222,6 +222,7 @@ __device__ double delta_range_u(const DecArgs& a, int64_t lh, int t_begin, int t
 // restricts it to heads whose chunked decode failed verification.
 template <typename Tout>
 __global__ void __launch_bounds__(kDThreads) k_dec_delta128(const DecArgs a, const uint32_t* only) {
+  if (payload_rejected(a)) return;
   const int64_t lh = blockIdx.x;
   if (only && !only[lh]) return;
   uint32_t flags = 0;
@@ -257,6 +258,7 @@ struct DeltaWs {
 
 template <typename Tout, int PASS>
 __global__ void __launch_bounds__(kDThreads) k_delta_chunk(const DecArgs a, DeltaWs w) {
+  if (payload_rejected(a)) return;
   const int64_t lh = blockIdx.x / w.nchunks;
   const int ch = (int)(blockIdx.x % w.nchunks);
   const int ntiles = (int)((a.g.T + kDT - 1) / kDT);

@@ -725,6 +725,7 @@ __device__ __forceinline__ void dec_flags(const float* y, bool groups_finite, ui
 // Direct decode: any width layout, contiguous or paged output, bf16 or fp32.
 template <int MODE, typename Tout, int G, int W>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128(const DecArgs a) {
+  if (payload_rejected(a)) return;
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows;
@@ -832,6 +833,7 @@ __host__ __device__ constexpr int dec_smem_bytes() {
 
 template <int MODE, int G, int W, bool PAGED>
 __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__ CUtensorMap omap, const DecArgs a) {
+  if (payload_rejected(a)) return;
   constexpr int NS = dec_stages<W>();
   constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<MODE, W, G>();
   extern __shared__ uint8_t smem_raw[];

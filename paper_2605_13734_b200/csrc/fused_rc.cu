@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedAr
 // which then decodes a zero stream (so warp-cooperative stores stay intact)
 __device__ __forceinline__ bool open_block(const FusedArgs& a, int64_t b, RcDec& d, int64_t& avail) {
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  bool ok = o1 >= o0 && o1 - o0 >= 8 && (a.payload_bytes < 0 || (int64_t)o1 <= a.payload_bytes);
+  bool ok = o1 >= o0 && o1 - o0 >= 8 && (a.payload_bytes < 0 || o1 <= (uint64_t)a.payload_bytes);
   if (ok) {
     const uint8_t* src = a.payload_in + o0;
     const uint32_t hdr = ((uint32_t)src[0] << 24) | ((uint32_t)src[1] << 16) | ((uint32_t)src[2] << 8) | src[3];

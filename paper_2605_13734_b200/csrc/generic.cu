@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(256) k_encode_fixup(EncArgs a) {
 // ------------------------------------------------------------ generic decode
 template <typename Tout>
 __global__ void __launch_bounds__(256) k_decode_generic(DecArgs a, int TT) {
+  if (payload_rejected(a)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const Geo& g = a.g;
   const int64_t C = g.C, T = g.T;
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(256) k_decode_generic(DecArgs a, int TT) {
 // in token order exactly like np.cumsum(dtype=float64) (transforms.py:72).
 template <typename Tout>
 __global__ void __launch_bounds__(128) k_decode_delta(DecArgs a) {
+  if (payload_rejected(a)) return;
   const Geo& g = a.g;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= g.LH * g.C) return;

@@ -38,6 +38,14 @@ struct DecArgs {
   int64_t page_tokens, layer_stride;
 };
 
+#ifdef __CUDACC__
+// codec none reads the caller's payload directly: when the length check that
+// runs first (k_check_payload) rejected it, the decode kernels read nothing
+__device__ __forceinline__ bool payload_rejected(const DecArgs& a) {
+  return a.g.codec == C_NONE && (*reinterpret_cast<const volatile uint32_t*>(a.status) & KVC_FLAG_CODEC);
+}
+#endif
+
 struct ClassBits {
   uint8_t b[4096];
 };

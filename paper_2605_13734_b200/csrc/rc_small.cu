@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(128) k_rc_small_decode(CodecArgs a) {
   const int64_t start = (b - st.first_block[si]) * a.g.block;
   const int n = (int)min(a.g.block, st.count[si] - start);
   const uint64_t o0 = a.offsets_in[b], o1 = a.offsets_in[b + 1];
-  if (o1 < o0 || o1 - o0 < 8 || (a.payload_bytes >= 0 && (int64_t)o1 > a.payload_bytes)) {
+  if (o1 < o0 || o1 - o0 < 8 || (a.payload_bytes >= 0 && o1 > (uint64_t)a.payload_bytes)) {
     atomicOr(a.status, KVC_FLAG_CODEC);
     return;
   }

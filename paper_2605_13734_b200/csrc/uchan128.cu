@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kUThreads, 3) k_enc_uchan128(const __grid_cons
 // ------------------------------------------------------------------ decode
 template <int W, bool AFFINE, typename Tout>
 __global__ void __launch_bounds__(kUThreads, 3) k_dec_uchan128(const DecArgs a) {
+  if (payload_rejected(a)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tile = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 15) & ~(uintptr_t)15);
   // [128 tokens][128 ch] Tout  (bf16: 32 KB, f32: 64 KB)
