@@ -105,14 +105,18 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
 
 /* Decode into a contiguous (L,H,T,C) tensor of the plan's out_dtype.
  * `payload_bytes` is the received payload length (checked like the
- * reference's trailing-byte rule, codecs.py:412-413 / :429-430); pass -1 for a
- * device-resident blob whose length is block_offsets[nblocks]. */
+ * reference's trailing-byte rule, codecs.py:412-413 / :429-430): every block
+ * offset is bounded by it, so any payload bytes and any offset table decode
+ * or raise KVC_FLAG_CODEC, never read outside [payload, payload+payload_bytes).
+ * Pass -1 for a device-resident blob this library encoded (its length is
+ * block_offsets[nblocks]): the offsets are then trusted, not bounded. */
 int kvc_decode(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
                const uint64_t* block_offsets, void* out, void* workspace, void* stream);
 
 /* Decode into a paged cache: element (l,h,t,c) lands at
  *   base + l*layer_stride + (block_table[t / page_tokens]*page_tokens + t % page_tokens)*H*C + h*C + c
- * (vLLM layout [num_pages, page_tokens, heads, channels] per layer; strides in elements). */
+ * (vLLM layout [num_pages, page_tokens, heads, channels] per layer; strides in elements).
+ * The block table is trusted: its entries must name pages inside page_base. */
 int kvc_decode_paged(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,
                      const uint64_t* block_offsets, void* page_base, const int32_t* block_table, int64_t page_tokens,
                      int64_t layer_stride, void* workspace, void* stream);
