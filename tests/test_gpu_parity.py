@@ -304,6 +304,42 @@ def test_parity_fuzz(k):
     assert_decoded(got, rec, sid, shape, in_f32=in_f32)
 
 
+@pytest.mark.parametrize("k", range(100))
+def test_parity_fuzz_bf16_out_and_paged(k):
+    """The production outputs on fuzzed cases: a bf16-output plan decodes the
+    same blob to exactly bf16(RN(fp32 decode)), and a paged decode (random
+    page size and page table, vLLM layout) holds the contiguous bf16 values."""
+    from paper_2605_13734_b200 import KVCodec
+
+    sid, shape, block, in_f32 = (_fuzz_case_fast if k % 2 else _fuzz_case)(1000 + k)
+    got32, rec, vb = run_case(sid, shape, seed=k, block=block, in_f32=in_f32)
+    assert_decoded(got32, rec, sid, shape, in_f32=in_f32)
+    L, H, T, C = shape
+    s = oracle.parse_id(sid)
+    _, imp = oracle.generate_kv(L, H, T, C, seed=k)
+    cls = oracle.classify_heads(imp, s.rho) if s.quant == "mixed" else (
+        oracle.layer_classes(imp, s.rho) if s.quant == "mixlayer" else None)
+    dt = torch.float32 if in_f32 else torch.bfloat16
+    kv = torch.from_numpy(vb).to(dt).cuda().contiguous()
+    codec = KVCodec(sid, shape, in_dtype=dt, out_dtype=torch.bfloat16, block_symbols=block)
+    blob = codec.encode(kv, head_classes=cls)
+    flat = codec.decode(blob)
+    codec.check(decoding=True)
+    want = torch.from_numpy(got32).to(torch.bfloat16).cuda()
+    assert torch.equal(flat.view(torch.int16), want.view(torch.int16)), ("bf16 out", sid, shape)
+    rng = np.random.default_rng(k)
+    P = int(rng.choice([1, 3, 16, 32, 64, 128]))
+    need = -(-T // P)
+    npages = need + int(rng.integers(0, 4))
+    table = torch.from_numpy(rng.permutation(npages)[:need].astype(np.int32)).cuda()
+    pages = torch.zeros(L * npages * P * H * C, dtype=torch.bfloat16, device="cuda")
+    codec.decode_paged(blob, pages, table, P, npages * P * H * C)
+    codec.check(decoding=True)
+    rows = (table.long()[:, None] * P + torch.arange(P, device="cuda")[None, :]).reshape(-1)[:T]
+    pv = pages.view(L, npages * P, H, C)[:, rows].permute(0, 2, 1, 3)
+    assert torch.equal(pv.view(torch.int16), flat.view(torch.int16)), ("paged", sid, shape, P)
+
+
 def test_f32_input_matches_reference_fixture():
     """fp32 (non-bf16) inputs: the golden whole-tensor blobs from the reference."""
     from golden_io import items, load
