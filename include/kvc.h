@@ -103,6 +103,15 @@ int64_t kvc_num_blocks(const kvc_plan* plan, const uint8_t* head_classes);
 int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
                uint64_t* block_offsets, void* workspace, void* stream);
 
+/* kvc_encode reading the KV straight from a paged cache (the layout of
+ * kvc_decode_paged: element (l,h,t,c) at
+ *   page_base + l*layer_stride + (block_table[t / page_tokens]*page_tokens + t % page_tokens)*H*C + h*C + c),
+ * in the plan's in_dtype.  The blob is byte-identical to kvc_encode of the
+ * gathered contiguous tensor, with no gather pass.  The block table is trusted. */
+int kvc_encode_paged(const kvc_plan* plan, const void* page_base, const int32_t* block_table, int64_t page_tokens,
+                     int64_t layer_stride, const uint8_t* head_classes, void* payload, void* metadata,
+                     uint64_t* block_offsets, void* workspace, void* stream);
+
 /* Decode into a contiguous (L,H,T,C) tensor of the plan's out_dtype.
  * `payload_bytes` is the received payload length (checked like the
  * reference's trailing-byte rule, codecs.py:412-413 / :429-430): every block

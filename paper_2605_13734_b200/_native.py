@@ -34,6 +34,7 @@ EXPORTS = (
     "kvc_static_payload_bytes",
     "kvc_num_blocks",
     "kvc_encode",
+    "kvc_encode_paged",
     "kvc_decode",
     "kvc_decode_paged",
     "kvc_read_status",
@@ -101,6 +102,8 @@ def lib() -> ctypes.CDLL:
     L.kvc_num_blocks.restype = I64
     L.kvc_encode.argtypes = [P, P, P, P, P, P, P, P]
     L.kvc_encode.restype = I32
+    L.kvc_encode_paged.argtypes = [P, P, P, I64, I64, P, P, P, P, P, P]
+    L.kvc_encode_paged.restype = I32
     L.kvc_decode.argtypes = [P, P, I64, P, P, P, P, P]
     L.kvc_decode.restype = I32
     L.kvc_decode_paged.argtypes = [P, P, I64, P, P, P, P, I64, I64, P, P]

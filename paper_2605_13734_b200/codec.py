@@ -212,6 +212,42 @@ class KVCodec:
             blob.nblocks = int(self._lib.kvc_num_blocks(self._h, cptr))
         return blob
 
+    def encode_paged(self, pages: torch.Tensor, block_table: torch.Tensor, page_tokens: int, layer_stride: int,
+                     head_classes=None, out: DeviceBlob | None = None,
+                     stream: torch.cuda.Stream | None = None) -> DeviceBlob:
+        """Encode straight from a paged cache (vLLM layout [pages, page_tokens,
+        H, C] per layer, the layout decode_paged writes): the blob is
+        byte-identical to encode() of the gathered (L,H,T,C) tensor."""
+        if pages.dtype != self.in_dtype or not pages.is_cuda or not pages.is_contiguous():
+            raise ValueError(f"pages must be a contiguous {self.in_dtype} CUDA tensor")
+        L, H, T, C = self.shape
+        if page_tokens < 1 or layer_stride < 0:
+            raise ValueError("page_tokens must be >= 1 and layer_stride >= 0")
+        need = -(-T // page_tokens)
+        bt = block_table
+        if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
+            bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
+        if bt.numel() < need:
+            raise ValueError(f"block_table has {bt.numel()} entries, {need} needed for {T} tokens")
+        arr, cptr = self._classes_arg(head_classes)
+        blob = out if out is not None else self.alloc_blob(arr)
+        if arr is not None:
+            blob.head_classes = arr.astype(bool).reshape(self.shape[:2])
+        N.check(
+            self._lib.kvc_encode_paged(
+                self._h, pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), cptr,
+                blob.payload.data_ptr(), blob.metadata.data_ptr() if self.metadata_bytes else blob.payload.data_ptr(),
+                _ptr(blob.offsets), self.workspace.data_ptr(), _stream_handle(stream),
+            )
+        )
+        if self.codec_kind == "none":
+            blob._nbytes = int(self._lib.kvc_static_payload_bytes(self._h, cptr))
+            blob.nblocks = 0
+        else:
+            blob._nbytes = None
+            blob.nblocks = int(self._lib.kvc_num_blocks(self._h, cptr))
+        return blob
+
     # ------------------------------------------------------------- decode
     def decode(self, blob: DeviceBlob, out: torch.Tensor | None = None,
                stream: torch.cuda.Stream | None = None, device_length: bool = False) -> torch.Tensor:

@@ -375,14 +375,17 @@ static void fill_common(const Plan& p, double& hk, double& hc) {
   hk = std::ldexp(1.0 / hc, 896);
 }
 
-int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
-               uint64_t* block_offsets, void* workspace, void* stream) {
+static int encode_impl(const kvc_plan* plan, const void* kv, int paged, const int32_t* block_table,
+                       int64_t page_tokens, int64_t layer_stride, const uint8_t* head_classes, void* payload,
+                       void* metadata, uint64_t* block_offsets, void* workspace, void* stream) {
   if (!plan) return fail(KVC_ERR_CONFIG, "plan is NULL");
   const Plan& p = plan->p;
   const Geo& g = p.g;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!kv || !payload || !metadata || !workspace) return fail(KVC_ERR_CONFIG, "NULL buffer");
   if (g.codec != C_NONE && !block_offsets) return fail(KVC_ERR_CONFIG, "block_offsets required for rle/entropy");
+  if (paged && (!block_table || page_tokens < 1 || layer_stride < 0))
+    return fail(KVC_ERR_CONFIG, "paged encode needs a block table, page_tokens >= 1 and layer_stride >= 0");
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   uint8_t* meta = reinterpret_cast<uint8_t*>(metadata);
   uint32_t* status = reinterpret_cast<uint32_t*>(ws + p.ws_status);
@@ -399,14 +402,27 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
       return cuda_fail(e, "classmap");
   }
   if ((e = launch_setup(g, meta, st, heads, s)) != cudaSuccess) return cuda_fail(e, "setup");
+  EncArgs a;
+  memset(&a, 0, sizeof a);
+  a.g = g;
+  a.kv = kv;
+  a.meta = meta;
+  a.paged = paged;
+  a.block_table = block_table;
+  a.page_tokens = page_tokens;
+  a.layer_stride = layer_stride;
   if (g.transform == T_AFFINE)
-    if ((e = launch_affine_calibrate(g, kv, meta, s)) != cudaSuccess) return cuda_fail(e, "affine");
+    if ((e = launch_affine_calibrate(a, s)) != cudaSuccess) return cuda_fail(e, "affine");
   if (fused_rc_applicable(g)) {
     // quantize + range code in one pass, then block offsets + gather
     FusedArgs f;
     memset(&f, 0, sizeof f);
     f.g = g;
     f.kv = kv;
+    f.paged = paged;
+    f.block_table = block_table;
+    f.page_tokens = page_tokens;
+    f.layer_stride = layer_stride;
     f.scales = reinterpret_cast<__half*>(meta);
     f.zeros = f.scales + g.ngroups;
     f.slots = ws + p.ws_slots;
@@ -432,12 +448,7 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
     if ((e = launch_codec_finish(c, s)) != cudaSuccess) return cuda_fail(e, "codec finish");
     return KVC_OK;
   }
-  EncArgs a;
-  memset(&a, 0, sizeof a);
-  a.g = g;
-  a.kv = kv;
   a.packed = g.codec == C_NONE ? reinterpret_cast<uint8_t*>(payload) : ws + p.ws_packed;
-  a.meta = meta;
   a.heads = heads;
   a.st = st;
   a.status = status;
@@ -482,6 +493,18 @@ int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes
     if ((e = launch_codec_encode(c, p.sm_count, s)) != cudaSuccess) return cuda_fail(e, "codec encode");
   }
   return KVC_OK;
+}
+
+int kvc_encode(const kvc_plan* plan, const void* kv, const uint8_t* head_classes, void* payload, void* metadata,
+               uint64_t* block_offsets, void* workspace, void* stream) {
+  return encode_impl(plan, kv, 0, nullptr, 0, 0, head_classes, payload, metadata, block_offsets, workspace, stream);
+}
+
+int kvc_encode_paged(const kvc_plan* plan, const void* page_base, const int32_t* block_table, int64_t page_tokens,
+                     int64_t layer_stride, const uint8_t* head_classes, void* payload, void* metadata,
+                     uint64_t* block_offsets, void* workspace, void* stream) {
+  return encode_impl(plan, page_base, 1, block_table, page_tokens, layer_stride, head_classes, payload, metadata,
+                     block_offsets, workspace, stream);
 }
 
 static int decode_impl(const kvc_plan* plan, const void* payload, int64_t payload_bytes, const void* metadata,

@@ -62,6 +62,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// paged cache view (64 ch, half, head, token row, layer), as make_paged_map:
+// one box = a run of tokens of one head inside one page
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int h, int r, int l, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(0), "r"(0), "r"(h), "r"(r), "r"(l), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ----------------------------------------------------------- bit packing
@@ -345,13 +354,28 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // one tile into ring slot s (thread 0): a 2D box, or for a paged cache
+  // (bf16, whole 64-token tiles of one head) one 5D box per page run of bt
+  // tokens -- the same 128B-swizzled half rows, at 1 KB-aligned offsets
+  auto issue = [&](int s, int64_t tile) {
+    mbar_expect_tx(&full[s], TB);
+    if (F32 || !a.paged) {
+      tma_load_2d(tiles + s * TB, &tmap, 0, (int)(tile * kBoxRows), &full[s]);
+      return;
+    }
+    const int64_t r0 = tile * kRows, lh = r0 / g.T, t0 = r0 - lh * g.T;
+    const int l = (int)(lh / g.H), h = (int)(lh - (int64_t)l * g.H);
+    const int bt = a.page_tokens < kRows ? (int)a.page_tokens : kRows;
+    for (int j = 0; j < kRows; j += bt) {
+      const int64_t t = t0 + j;
+      const int64_t prow = (int64_t)a.block_table[t / a.page_tokens] * a.page_tokens + t % a.page_tokens;
+      tma_load_5d(tiles + s * TB + j * 256, &tmap, h, (int)prow, l, &full[s]);
+    }
+  };
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
-      if (tile < ntiles) {
-        mbar_expect_tx(&full[s], TB);
-        tma_load_2d(tiles + s * TB, &tmap, 0, (int)(tile * kBoxRows), &full[s]);
-      }
+      if (tile < ntiles) issue(s, tile);
     }
   }
   __half* scales = reinterpret_cast<__half*>(a.meta);
@@ -395,8 +419,9 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       if (tid >= 2) {
         load_half(tb, tid - 2, pv);
       } else if (valid && t > 0) {
+        const int64_t prev = F32 ? (row - 1) * 128 + half * 64 : out_index(a, lh, t - 1, half * 64);
         const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) +
-                                                          ((row - 1) * 128 + half * 64) * (F32 ? 4 : 2));
+                                                          prev * (F32 ? 4 : 2));
 #pragma unroll
         for (int k = 0; k < NW / 4; ++k) {
           uint4 c = __ldg(src + k);
@@ -409,8 +434,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       const int64_t next = tile + (int64_t)NS * gridDim.x;
       if (next < ntiles) {
         fence_proxy_async();
-        mbar_expect_tx(&full[s], TB);
-        tma_load_2d(tiles + s * TB, &tmap, 0, (int)(next * kBoxRows), &full[s]);
+        issue(s, next);
       }
     }
     // invalid tail rows run the same code (shuffles need the full warp) but
@@ -1066,19 +1090,30 @@ cudaError_t launch_enc_t(const CUtensorMap& map, const EncArgs& a, int sm_count,
 // paged cache [pages, page_tokens, H, 128] per layer (layer_stride elements)
 // as a 5-D view (64 channels, half, head, token row, layer); the box is bt
 // tokens of one head, the same 128B-swizzled smem rows as the contiguous map
-bool make_paged_map(CUtensorMap* map, const DecArgs& a, int bt) {
+bool make_paged_map(CUtensorMap* map, void* base, const Geo& g, int64_t layer_stride, int bt) {
   auto fn = get_encode_fn();
   if (!fn) return false;
-  const int64_t row_elems = a.g.H * 128;
-  const int64_t rows = a.layer_stride / row_elems;  // token rows per layer in the pool
-  cuuint64_t dims[5] = {64, 2, (cuuint64_t)a.g.H, (cuuint64_t)rows, (cuuint64_t)a.g.L};
-  cuuint64_t strides[4] = {128, 256, (cuuint64_t)row_elems * 2, (cuuint64_t)a.layer_stride * 2};
+  const int64_t row_elems = g.H * 128;
+  const int64_t rows = layer_stride / row_elems;  // token rows per layer in the pool
+  cuuint64_t dims[5] = {64, 2, (cuuint64_t)g.H, (cuuint64_t)rows, (cuuint64_t)g.L};
+  cuuint64_t strides[4] = {128, 256, (cuuint64_t)row_elems * 2, (cuuint64_t)layer_stride * 2};
   cuuint32_t box[5] = {64, 2, 1, (cuuint32_t)bt, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, a.out, dims, strides, box, estr,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// paged encode input through the 5D map: whole 64-token tiles of one head,
+// page runs that tile 64 tokens (4..64, or multiples of 64), a per-layer pool
+// extent with 16-byte aligned strides
+bool paged_input_ok(const EncArgs& a) {
+  const int64_t pt = a.page_tokens, row_elems = a.g.H * 128;
+  if (a.g.T % kRows != 0 || pt < 4 || (pt < kRows ? kRows % pt : pt % kRows) != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(a.kv) & 15u) != 0) return false;
+  if (a.layer_stride <= 0 || a.layer_stride % row_elems != 0 || (a.layer_stride * 2) % 16 != 0) return false;
+  return a.layer_stride / row_elems < (1ll << 31);
 }
 
 template <typename Tout, int W>
@@ -1104,7 +1139,7 @@ cudaError_t launch_dec_gw(const DecArgs& a, int sm_count, cudaStream_t s) {
   if constexpr (sizeof(Tout) == 2 && W != 0) {
     CUtensorMap omap;
     const bool mapped = dec_staged_ok<Tout, W>(a) &&
-                        (a.paged ? make_paged_map(&omap, a, (int)std::min<int64_t>(a.page_tokens, 16))
+                        (a.paged ? make_paged_map(&omap, a.out, a.g, a.layer_stride, (int)std::min<int64_t>(a.page_tokens, 16))
                                  : make_input_map(&omap, a.out, a.g.LH * a.g.T));
     if (mapped) {
       auto k = a.paged ? k_dec128r<MODE, G, W, true> : k_dec128r<MODE, G, W, false>;
@@ -1169,8 +1204,13 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
   const int64_t nrows = a.g.LH * a.g.T;
   if ((f32 ? 4 : 2) * nrows >= (1ll << 31)) return launch_encode_generic(a, s);
   CUtensorMap map;
-  if (!(f32 ? make_input_map_f32(&map, a.kv, nrows) : make_input_map(&map, a.kv, nrows)))
+  if (a.paged) {
+    if (f32 || !paged_input_ok(a) || !make_paged_map(&map, const_cast<void*>(a.kv), a.g, a.layer_stride,
+                                                     (int)std::min<int64_t>(a.page_tokens, kRows)))
+      return launch_encode_generic(a, s);
+  } else if (!(f32 ? make_input_map_f32(&map, a.kv, nrows) : make_input_map(&map, a.kv, nrows))) {
     return launch_encode_generic(a, s);
+  }
   ProfScope ps("encode_fast128", s);
   return f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
 }

@@ -250,24 +250,30 @@ __device__ __forceinline__ void stage_value(uint8_t* tile, int row, int col, int
 // ------------------------------------------------------------- per token
 // one block's groups; FULL = every lane of the warp codes a full block (the
 // warp-uniform votes then use a constant mask, with no divergence checks)
-template <int W, bool FULL>
+template <int W, bool FULL, bool PAGED>
 __device__ __forceinline__ void tok_encode_groups(const FusedArgs& a, const uint4* src, int64_t r0, int ngr, RcEnc& e,
                                                   SModel<W>& m, uint32_t& flags, bool& nonfinite) {
   const float rl = a.rl[W];
   uint64_t sacc = 0, zacc = 0;
+  const uint4* rp = src;  // PAGED: the current token row, from its page
 #pragma unroll 1
   for (int gi = 0; gi < ngr; ++gi) {
     const unsigned mask = FULL ? 0xffffffffu : __activemask();
     if constexpr (FULL) __syncwarp();  // proves convergence: no BRA.DIV before each vote
+    if (PAGED && (gi & 3) == 0) {
+      const int64_t r = r0 + (gi >> 2), lh = r / a.g.T;
+      rp = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + out_index(a, lh, r - lh * a.g.T, 0));
+    }
+    const uint4* gp = PAGED ? rp + (gi & 3) * 4 : src + gi * 4;
     uint32_t wv[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint4 v = __ldcs(src + gi * 4 + k);  // read once: evict-first, keeps the coded slots in L2
+      const uint4 v = __ldcs(gp + k);  // read once: evict-first, keeps the coded slots in L2
       wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
     }
-    if (gi + 1 < ngr) {  // next group's 64 bytes
-      prefetch_l1(src + gi * 4 + 4);
-      prefetch_l1(src + gi * 4 + 6);
+    if (gi + 1 < ngr && (!PAGED || (gi & 3) != 3)) {  // next group's 64 bytes (paged: within the row)
+      prefetch_l1(gp + 4);
+      prefetch_l1(gp + 6);
     }
     float mn, mx;
     minmax_words(wv, mn, mx);
@@ -312,10 +318,12 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedAr
   // the activemask variant
   const int64_t wlast = b - (threadIdx.x & 31) + 31;
   const bool full = wlast < nblocks - 1 || (wlast == nblocks - 1 && nrows % R == 0);
-  if (full)
-    tok_encode_groups<W, true>(a, src, r0, nr * 4, e, m, flags, nonfinite);
+  if (a.paged)
+    tok_encode_groups<W, false, true>(a, src, r0, nr * 4, e, m, flags, nonfinite);
+  else if (full)
+    tok_encode_groups<W, true, false>(a, src, r0, nr * 4, e, m, flags, nonfinite);
   else
-    tok_encode_groups<W, false>(a, src, r0, nr * 4, e, m, flags, nonfinite);
+    tok_encode_groups<W, false, false>(a, src, r0, nr * 4, e, m, flags, nonfinite);
   const uint32_t len = e.finish();
   *reinterpret_cast<uint32_t*>(slot) = __byte_perm(len, 0, 0x0123);
   a.sizes[b] = (uint64_t)len + 4;
@@ -450,6 +458,11 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
   // lane's token row for group gi: token t0 + 32 gi + lane, channels c0 .. c0+31
   const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) +
                                                     ((cm.lh * g.T + t0 + lane) * 128 + c0));
+  // paged cache: lane's token row of group gi from its page
+  const auto paged_row = [&](int gi) {
+    return reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) +
+                                          out_index(a, cm.lh, t0 + (int64_t)gi * 32 + lane, c0));
+  };
   uint8_t* slot = a.slots + cm.b * a.slot_bytes;
   RcEnc e;
   e.init(reinterpret_cast<uint32_t*>(slot + 4));
@@ -463,13 +476,14 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
   uint64_t sacc = 0, zacc = 0;
 #pragma unroll 1
   for (int gi = 0; gi < ngr; ++gi) {
-    const uint4* rowp = src + (int64_t)gi * 32 * 16;  // 32 tokens = 32 * 256 B
+    const uint4* rowp = a.paged ? paged_row(gi) : src + (int64_t)gi * 32 * 16;  // 32 tokens = 32 * 256 B
     uint4 v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __ldcs(rowp + k);  // read once (evict-first)
     if (gi + 1 < ngr) {
-      prefetch_l1(rowp + 32 * 16);
-      prefetch_l1(rowp + 32 * 16 + 2);
+      const uint4* nx = a.paged ? paged_row(gi + 1) : rowp + 32 * 16;
+      prefetch_l1(nx);
+      prefetch_l1(nx + 2);
     }
     // transpose through shared memory: lane l holds token l's 32 channels and
     // writes them down column l; row c then holds channel c0+c's 32 tokens

@@ -99,14 +99,17 @@ __global__ void k_write_classmap(ClassBits cb, uint8_t* dst, int nbytes) {
 // mu = f16(0.5*(max+min)), a = f16(min(2/(max-min), 65504)) over the first
 // min(T,128) tokens of each (layer, head, channel).  DESIGN.md §3 (extension).
 template <typename Tin>
-__global__ void k_affine_calibrate(Geo g, const Tin* kv, uint8_t* meta) {
+__global__ void k_affine_calibrate(const EncArgs a) {
+  const Geo& g = a.g;
+  const Tin* kv = reinterpret_cast<const Tin*>(a.kv);
+  uint8_t* meta = a.meta;
   const int64_t lh = blockIdx.x;
   const int64_t nt = g.T < kAffinePrefix ? g.T : kAffinePrefix;
   uint8_t* aff = meta + g.meta_affine_off;  // mu16[LH*C] || a16[LH*C]
   for (int64_t c = threadIdx.x; c < g.C; c += blockDim.x) {
     float mx = -INFINITY, mn = INFINITY;
     for (int64_t t = 0; t < nt; ++t) {
-      float v = load_f32(kv, (lh * g.T + t) * g.C + c);
+      float v = load_f32(kv, out_index(a, lh, t, c));
       mx = fmaxf(mx, v);
       mn = fminf(mn, v);
     }
@@ -167,18 +170,28 @@ __device__ void encode_tile(const EncArgs& a, int TT, int64_t lh, int64_t t0, in
   float* prev = y + (int64_t)TT * C;          // [C]
   uint8_t* sym = reinterpret_cast<uint8_t*>(prev + C);  // quant-ordered symbols
   double* fw = reinterpret_cast<double*>(smem + (((int64_t)TT * C * 5 + C * 4 + 15) & ~15ll));
-  const Tin* src = reinterpret_cast<const Tin*>(a.kv) + (lh * T + t0) * C;
+  const Tin* kv = reinterpret_cast<const Tin*>(a.kv);
+  const Tin* src = kv + (lh * T + t0) * C;
   uint32_t flags = 0;
 
   float nanacc = 0.0f;
-  for (int64_t i = threadIdx.x; i < (int64_t)nt * C; i += blockDim.x) {
-    float v = load_f32(src, i);
-    nanacc = __fmaf_rn(v, 0.0f, nanacc);
-    y[i] = v;
+  if (!a.paged) {
+    for (int64_t i = threadIdx.x; i < (int64_t)nt * C; i += blockDim.x) {
+      float v = load_f32(src, i);
+      nanacc = __fmaf_rn(v, 0.0f, nanacc);
+      y[i] = v;
+    }
+  } else {  // paged input: each token row from its page
+    for (int64_t i = threadIdx.x; i < (int64_t)nt * C; i += blockDim.x) {
+      const int64_t tr = i / C;
+      float v = load_f32(kv, out_index(a, lh, t0 + tr, i - tr * C));
+      nanacc = __fmaf_rn(v, 0.0f, nanacc);
+      y[i] = v;
+    }
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   if (g.transform == T_DELTA && t0 > 0)
-    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) prev[c] = load_f32(src - C, c);
+    for (int64_t c = threadIdx.x; c < C; c += blockDim.x) prev[c] = load_f32(kv, out_index(a, lh, t0 - 1, c));
   __syncthreads();
 
   // ---- transform (transforms.py:50-64; affine: extension)
@@ -294,13 +307,14 @@ __global__ void __launch_bounds__(256) k_encode_generic(EncArgs a, int TT) {
 // whose fast rounding it could not prove exact, fast128.cu): each CTA takes
 // list entries in turn and overwrites the row's bytes, scales and zeros.  The
 // count is read on the device, so the launch never waits on the host.
+template <typename Tin>
 __global__ void __launch_bounds__(256) k_encode_fixup(EncArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t n = *a.fix_count;
   for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
     const int64_t row = a.fix_rows[e];
     const int64_t lh = row / a.g.T;
-    encode_tile<__nv_bfloat16>(a, 1, lh, row - lh * a.g.T, 1, smem);
+    encode_tile<Tin>(a, 1, lh, row - lh * a.g.T, 1, smem);
     __syncthreads();
   }
 }
@@ -463,8 +477,13 @@ cudaError_t launch_encode_fixup(const EncArgs& a, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   ProfScope ps("encode_fixup", s);
-  cudaFuncSetAttribute(k_encode_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_encode_fixup<<<(unsigned)(2 * sms), 256, sm, s>>>(a);
+  if (a.g.in_dtype == KVC_DTYPE_BF16) {
+    cudaFuncSetAttribute(k_encode_fixup<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_encode_fixup<__nv_bfloat16><<<(unsigned)(2 * sms), 256, sm, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_encode_fixup<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_encode_fixup<float><<<(unsigned)(2 * sms), 256, sm, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -506,13 +525,14 @@ cudaError_t launch_write_classmap(const ClassBits& cb, uint8_t* dst, int nbytes,
   return cudaGetLastError();
 }
 
-cudaError_t launch_affine_calibrate(const Geo& g, const void* kv, uint8_t* meta, cudaStream_t s) {
+cudaError_t launch_affine_calibrate(const EncArgs& a, cudaStream_t s) {
+  const Geo& g = a.g;
   unsigned thr = (unsigned)(g.C < 256 ? ((g.C + 31) / 32) * 32 : 256);
   ProfScope ps("affine_calibrate", s);
   if (g.in_dtype == KVC_DTYPE_BF16)
-    k_affine_calibrate<__nv_bfloat16><<<(unsigned)g.LH, thr, 0, s>>>(g, reinterpret_cast<const __nv_bfloat16*>(kv), meta);
+    k_affine_calibrate<__nv_bfloat16><<<(unsigned)g.LH, thr, 0, s>>>(a);
   else
-    k_affine_calibrate<float><<<(unsigned)g.LH, thr, 0, s>>>(g, reinterpret_cast<const float*>(kv), meta);
+    k_affine_calibrate<float><<<(unsigned)g.LH, thr, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,10 @@ struct EncArgs {
   float rl[9];      // RN32(1 / (2^w - 1))
   int32_t* fix_rows;    // fused Hadamard encode: rows left to the exact fixup pass
   uint32_t* fix_count;
+  // paged input (kvc_encode_paged): row (lh, t) of kv at out_index(a, lh, t, 0)
+  int paged;
+  const int32_t* block_table;
+  int64_t page_tokens, layer_stride;
 };
 
 struct DecArgs {
@@ -76,7 +80,7 @@ struct CodecArgs {
 // block straight to KV (decode); no packed-symbol round trip through HBM.
 struct FusedArgs {
   Geo g;
-  const void* kv;              // encode input, (L,H,T,C) bf16
+  const void* kv;              // encode input, (L,H,T,C) bf16, contiguous or paged (out_index)
   __half* scales;              // encode: metadata scales / zeros out
   __half* zeros;
   const __half* scales_in;     // decode: metadata in
@@ -88,7 +92,7 @@ struct FusedArgs {
   const uint64_t* offsets_in;
   int64_t payload_bytes;
   void* out;                   // decode output (contiguous or paged)
-  int paged;
+  int paged;                   // encode: kv is paged; decode: out is paged
   const int32_t* block_table;
   int64_t page_tokens, layer_stride;
   uint32_t* status;
@@ -110,6 +114,9 @@ inline void set_max_dyn_smem(int bytes) {
   }
 }
 
+// element index of (lh, t, c) in the KV cache: contiguous (L,H,T,C), or the
+// paged layout [pages, page_tokens, H, C] per layer (the decode output, and
+// the encode input of kvc_encode_paged)
 template <class A>
 __device__ __forceinline__ int64_t out_index(const A& a, int64_t lh, int64_t t, int64_t c) {
   if (!a.paged) return (lh * a.g.T + t) * a.g.C + c;
@@ -120,7 +127,7 @@ __device__ __forceinline__ int64_t out_index(const A& a, int64_t lh, int64_t t, 
 
 cudaError_t launch_setup(const Geo& g, const uint8_t* meta, StreamTab* st, HeadEntry* heads, cudaStream_t s);
 cudaError_t launch_write_classmap(const ClassBits& cb, uint8_t* dst, int nbytes, cudaStream_t s);
-cudaError_t launch_affine_calibrate(const Geo& g, const void* kv, uint8_t* meta, cudaStream_t s);
+cudaError_t launch_affine_calibrate(const EncArgs& a, cudaStream_t s);
 cudaError_t launch_encode_generic(const EncArgs& a, cudaStream_t s);
 cudaError_t launch_encode_fixup(const EncArgs& a, cudaStream_t s);
 cudaError_t launch_decode_generic(const DecArgs& a, cudaStream_t s);

@@ -382,7 +382,7 @@ bool uchan128_applicable(const Geo& g) {
 }
 
 cudaError_t launch_encode_uchan128(const EncArgs& a, int sm_count, cudaStream_t s) {
-  if (a.g.in_dtype != KVC_DTYPE_BF16 || a.g.LH * a.g.T >= (1ll << 31)) return launch_encode_generic(a, s);
+  if (a.g.in_dtype != KVC_DTYPE_BF16 || a.g.LH * a.g.T >= (1ll << 31) || a.paged) return launch_encode_generic(a, s);
   auto fn = encode_fn();
   if (!fn) return launch_encode_generic(a, s);
   CUtensorMap map;

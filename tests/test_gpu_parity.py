@@ -445,10 +445,12 @@ def test_fp16_overflow_group_matches_reference_and_decode_raises(sid):
         codec.check(decoding=True)
 
 
-def test_hadamard_fast_path_adversarial_rows_are_exact():
+@pytest.mark.parametrize("in_f32", [False, True])
+def test_hadamard_fast_path_adversarial_rows_are_exact(in_f32):
     """The fused Hadamard encode leaves rows with zeros, tiny / huge
     magnitudes or near-midpoint results to the exact fixup pass
-    (k_encode_fixup); every row must still match the reference bit for bit."""
+    (k_encode_fixup); every row must still match the reference bit for bit,
+    for bf16 and for float32 (not bf16-exact) inputs."""
     shape = (1, 2, 64, 128)
     rng = np.random.default_rng(31)
     v = rng.normal(size=shape).astype(np.float32)
@@ -461,9 +463,12 @@ def test_hadamard_fast_path_adversarial_rows_are_exact():
     v[0, 1, 6, 7] = -3.0e-39                          # one tiny value in a normal row
     for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=2,g=64;c=entropy"):
         tb, vb = bf16_exact(v)
+        if in_f32:
+            vb = v
+            tb = torch.from_numpy(v)
         ref = oracle.encode_blob(vb, None, sid, block=256)
         from paper_2605_13734_b200 import KVCodec
-        codec = KVCodec(sid, shape, out_dtype=torch.float32, block_symbols=256)
+        codec = KVCodec(sid, shape, in_dtype=tb.dtype, out_dtype=torch.float32, block_symbols=256)
         blob = codec.encode(tb.cuda())
         codec.check()
         assert blob.metadata_bytes() == ref["metadata"], sid
