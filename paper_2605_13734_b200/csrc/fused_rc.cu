@@ -295,14 +295,23 @@ __device__ __forceinline__ void tok_encode_groups(const FusedArgs& a, const uint
 template <int W>
 __global__ void __launch_bounds__(kFThreads, 8) k_fused_tok_encode(const FusedArgs a) {
   const Geo& g = a.g;
-  const int64_t b = (int64_t)blockIdx.x * kFThreads + threadIdx.x;
-  if (b > a.max_blocks) return;
+  const int64_t gt = (int64_t)blockIdx.x * kFThreads + threadIdx.x;
+  if (gt > a.max_blocks) return;
   const int64_t nrows = g.LH * g.T;
   const int R = (int)(g.block / 128);
   const int64_t nblocks = (nrows + R - 1) / R;
-  if (b >= nblocks) {
-    a.sizes[b] = 0;
+  if (gt >= nblocks) {
+    a.sizes[gt] = 0;
     return;
+  }
+  // paged input with whole blocks per head: threads take blocks token-range
+  // major (l, token block, head), so a warp reads every head of its tokens
+  // (whole 2 KB rows of the page pool); block b's output is b's either way
+  int64_t b = gt;
+  if (a.paged && g.T % R == 0) {
+    const int64_t nbh = g.T / R, per_layer = g.H * nbh, l = gt / per_layer, rem = gt - l * per_layer;
+    const int64_t tb = rem / g.H, h = rem - tb * g.H;
+    b = (l * g.H + h) * nbh + tb;
   }
   const int64_t r0 = b * R;
   const int nr = (int)min((int64_t)R, nrows - r0);
@@ -450,7 +459,14 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
     if (gt <= a.max_blocks) a.sizes[gt] = 0;
     return;
   }
-  const ChanMap cm = chan_map(gt, nbt);
+  // paged input: (l, token chunk, head, channel) order -- the warps in flight
+  // cover every head of a token range (whole 2 KB rows of the page pool)
+  int64_t gm = gt;
+  if (a.paged) {
+    const int64_t c = gt & 127, q = gt >> 7, h = q % g.H, q2 = q / g.H, tc = q2 % nbt, l = q2 / nbt;
+    gm = ((l * g.H + h) * nbt + tc) * 128 + c;
+  }
+  const ChanMap cm = chan_map(gm, nbt);
   const int lane = threadIdx.x & 31;
   const int c0 = cm.c - lane;
   uint8_t* tile = tiles[threadIdx.x >> 5];
