@@ -14,7 +14,9 @@ three stages run concurrently on different engines:
                         the device-side length)
 
 chained by CUDA events, so chunk i's transfer and decode overlap chunk i+1's
-encode.  Each chunk is an independent blob of its (l, H, T, C) slab — the same
+encode.  `run_paged` is the KV-connector form: source and destination are
+paged caches (vLLM layout), read by kvc_encode_paged and written by
+kvc_decode_paged, so no gather or scatter pass touches the KV.  Each chunk is an independent blob of its (l, H, T, C) slab — the same
 per-layer sharding as distributed.py — so the decoded KV equals a whole-tensor
 decode bit for bit.
 """
@@ -97,22 +99,65 @@ class PipelinedKVTransfer:
             raise ValueError("kv must be the transfer's shape on the source device")
         if out is None:
             out = torch.empty(self.shape, dtype=self.out_dtype, device=self.dst)
+
+        def enc(i, l0, l1, cls, blob):
+            self.enc[i].encode(kv[l0:l1], head_classes=cls, out=blob, stream=self.s_enc)
+
+        def dec(i, l0, l1, blob):
+            self.dec[i].decode(blob, out=out[l0:l1], stream=self.s_dec, device_length=blob.offsets is not None)
+
+        self._pipeline(kv, out, enc, dec, head_classes)
+        return out
+
+    def run_paged(self, src_pages: torch.Tensor, src_table: torch.Tensor, dst_pages: torch.Tensor,
+                  dst_table: torch.Tensor, page_tokens: int, src_layer_stride: int, dst_layer_stride: int,
+                  head_classes=None) -> torch.Tensor:
+        """The KV-connector form: compress straight from the source GPU's
+        paged cache (kvc_encode_paged) and decompress straight into the
+        destination's (kvc_decode_paged), both vLLM layout [pages,
+        page_tokens, H, C] per layer with their own block tables; layer
+        chunk [l0, l1) of a pool starts l0 * layer_stride elements in."""
+        if src_pages.device != self.src or dst_pages.device != self.dst:
+            raise ValueError("page pools must live on the transfer's source / destination devices")
+        if not (src_pages.is_contiguous() and dst_pages.is_contiguous()):
+            raise ValueError("page pools must be contiguous")
+        L = self.shape[0]
+        if src_pages.numel() < L * src_layer_stride or dst_pages.numel() < L * dst_layer_stride:
+            raise ValueError("page pool smaller than layers x layer_stride")
+        sflat, dflat = src_pages.view(-1), dst_pages.view(-1)
+        st = src_table.to(device=self.src, dtype=torch.int32).contiguous()
+        dt = dst_table.to(device=self.dst, dtype=torch.int32).contiguous()
+
+        def enc(i, l0, l1, cls, blob):
+            self.enc[i].encode_paged(sflat[l0 * src_layer_stride:], st, page_tokens, src_layer_stride,
+                                     head_classes=cls, out=blob, stream=self.s_enc)
+
+        def dec(i, l0, l1, blob):
+            self.dec[i].decode_paged(blob, dflat[l0 * dst_layer_stride:], dt, page_tokens, dst_layer_stride,
+                                     stream=self.s_dec, device_length=blob.offsets is not None)
+
+        self._pipeline(src_pages, dst_pages, enc, dec, head_classes, keep=(st, dt))
+        return dst_pages
+
+    def _pipeline(self, src_t: torch.Tensor, dst_t: torch.Tensor, enc, dec, head_classes, keep=()) -> None:
         cur_src = torch.cuda.current_stream(self.src)
         cur_dst = torch.cuda.current_stream(self.dst)
-        # work already queued by the caller: kv's producer on the source, and
-        # any pending use of `out` (a reused KV slot) on the destination
+        # work already queued by the caller: the source's producer, and any
+        # pending use of the destination (a reused KV slot or page)
         self.s_enc.wait_stream(cur_src)
         self.s_copy.wait_stream(cur_dst)
         self.s_dec.wait_stream(cur_dst)
-        kv.record_stream(self.s_enc)
-        out.record_stream(self.s_dec)
+        src_t.record_stream(self.s_enc)
+        dst_t.record_stream(self.s_dec)
+        for t in keep:  # block tables built here: alive until their kernels ran
+            t.record_stream(self.s_enc if t.device == self.src else self.s_dec)
         for i, (l0, l1) in enumerate(self.chunks):
             cls = None if head_classes is None else head_classes[l0:l1]
             src_blob, dst_blob = self.tx_src[i], self.tx_dst[i]
             with torch.cuda.device(self.src):
                 # the previous run's copy of this chunk has read its wire buffer
                 self.s_enc.wait_event(self.ev_copy[i])
-                self.enc[i].encode(kv[l0:l1], head_classes=cls, out=src_blob, stream=self.s_enc)
+                enc(i, l0, l1, cls, src_blob)
                 self.ev_enc[i].record(self.s_enc)
                 self.s_copy.wait_event(self.ev_enc[i])
                 self.s_copy.wait_event(self.ev_dec[i])  # ... and its decode is done with the dst buffer
@@ -130,14 +175,12 @@ class PipelinedKVTransfer:
             dst_blob._nbytes = src_blob._nbytes
             with torch.cuda.device(self.dst):
                 self.s_dec.wait_event(self.ev_copy[i])
-                self.dec[i].decode(dst_blob, out=out[l0:l1], stream=self.s_dec,
-                                   device_length=dst_blob.offsets is not None)
+                dec(i, l0, l1, dst_blob)
                 self.ev_dec[i].record(self.s_dec)
         cur_dst.wait_stream(self.s_dec)
-        # the caller may free or overwrite kv once its own stream moves on
+        # the caller may free or overwrite the source once its own stream moves on
         cur_src.wait_stream(self.s_enc)
         cur_src.wait_stream(self.s_copy)
-        return out
 
     def check(self) -> None:
         """Synchronise both ends and raise for device-side errors."""

@@ -49,3 +49,58 @@ def test_two_gpus():
     tx.check()
     torch.cuda.synchronize(1)
     assert got.device.index == 1 and torch.equal(got.cpu(), want.cpu())
+
+
+def _pool(kv, P, seed, device):
+    """Scatter kv (L,H,T,C) into a paged pool [L, pages*P, H, C] (random table)."""
+    import numpy as np
+
+    L, H, T, C = kv.shape
+    need = -(-T // P)
+    npages = need + 2
+    table = torch.from_numpy(np.random.default_rng(seed).permutation(npages)[:need].astype(np.int32)).to(device)
+    pool = torch.zeros((L, npages * P, H, C), dtype=kv.dtype, device=device)
+    rows = (table.long()[:, None] * P + torch.arange(P, device=device)[None, :]).reshape(-1)[:T]
+    pool[:, rows] = kv.to(device).permute(0, 2, 1, 3)
+    return pool, table, rows, npages * P * H * C
+
+
+@pytest.mark.parametrize("sid", ["t=hadamard;q=uniform,b=4,g=32;c=none", "t=identity;q=uniform,b=2,g=32;c=entropy",
+                                 "t=affine;q=uniform,b=8,g=32;c=entropy"])
+def test_loopback_paged_connector(sid):
+    """Paged source cache -> encode_paged -> copy -> decode_paged into a
+    differently paged destination equals the direct contiguous decode."""
+    from paper_2605_13734_b200 import KVCodec
+    from paper_2605_13734_b200.transfer import PipelinedKVTransfer
+
+    shape = (5, 2, 1024, 128)
+    kv = _kv(shape, 8).cuda()
+    ref = KVCodec(sid, shape)
+    want = ref.decode(ref.encode(kv))
+    src, st, _, sstride = _pool(kv, 16, 1, "cuda:0")
+    dst, dt, drows, dstride = _pool(torch.zeros_like(kv), 16, 2, "cuda:0")
+    tx = PipelinedKVTransfer(sid, shape, 0, 0, chunk_layers=2)
+    for _ in range(2):
+        tx.run_paged(src, st, dst, dt, 16, sstride, dstride)
+        tx.check()
+        torch.cuda.synchronize()
+        assert torch.equal(dst[:, drows].permute(0, 2, 1, 3), want), sid
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_two_gpus_paged_connector():
+    from paper_2605_13734_b200 import KVCodec
+    from paper_2605_13734_b200.transfer import PipelinedKVTransfer
+
+    sid = "t=hadamard;q=uniform,b=4,g=32;c=none"
+    shape = (4, 2, 2048, 128)
+    kv = _kv(shape, 9).cuda(0)
+    ref = KVCodec(sid, shape)
+    want = ref.decode(ref.encode(kv)).cpu()
+    src, st, _, sstride = _pool(kv, 16, 3, "cuda:0")
+    dst, dt, drows, dstride = _pool(torch.zeros_like(kv), 16, 4, "cuda:1")
+    tx = PipelinedKVTransfer(sid, shape, 0, 1, chunk_layers=1)
+    tx.run_paged(src, st, dst, dt, 16, sstride, dstride)
+    tx.check()
+    torch.cuda.synchronize(1)
+    assert torch.equal(dst[:, drows].permute(0, 2, 1, 3).cpu(), want)
