@@ -556,7 +556,9 @@ cudaError_t launch_copy_device_length(void* dst, const void* src, const uint64_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (max_bytes / 16 + 255) / 256 + 1;
-  const int64_t cap = (int64_t)sms * 4;
+  // one CTA per SM moves bytes at link speed and leaves the SMs to the
+  // encoder running beside it (pipelined transfers)
+  const int64_t cap = (int64_t)sms;
   ProfScope ps("copy_device_length", s);
   k_copy_device_length<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(
       reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), nbytes_dev, max_bytes);

@@ -82,15 +82,21 @@ class PipelinedKVTransfer:
         with torch.cuda.device(self.dst):
             self.s_dec = torch.cuda.Stream(self.dst)
             self.ev_dec = [torch.cuda.Event() for _ in self.chunks]
-        # a device "length" larger than any buffer: fixed-size copies go
-        # through the same kernel, ordered on the copy stream
-        self._big = torch.full((1,), 1 << 62, dtype=torch.int64, device=self.src)
         torch.cuda.synchronize(self.src)
 
     def _copy(self, dst: torch.Tensor, src: torch.Tensor, len_ptr: int, max_bytes: int) -> None:
+        """Length known on the device only (entropy / rle payloads): the
+        copy kernel reads it there, so nothing syncs to the host."""
         if max_bytes > 0:
             N.check(N.lib().kvc_copy_device_length(dst.data_ptr(), src.data_ptr(), len_ptr, int(max_bytes),
                                                    _stream_handle(self.s_copy)))
+
+    def _dma(self, dst: torch.Tensor, src: torch.Tensor, nbytes: int) -> None:
+        """Length known on the host: a copy-engine peer copy, which leaves the
+        source GPU's SMs to the encoder of the next chunk."""
+        if nbytes > 0:
+            with torch.cuda.stream(self.s_copy):
+                dst[:nbytes].copy_(src[:nbytes], non_blocking=True)
 
     def run(self, kv: torch.Tensor, out: torch.Tensor | None = None, head_classes=None) -> torch.Tensor:
         """Start the pipelined transfer; returns the dst tensor (ordered on
@@ -161,15 +167,14 @@ class PipelinedKVTransfer:
                 self.ev_enc[i].record(self.s_enc)
                 self.s_copy.wait_event(self.ev_enc[i])
                 self.s_copy.wait_event(self.ev_dec[i])  # ... and its decode is done with the dst buffer
-                big = self._big.data_ptr()
-                self._copy(dst_blob.metadata, src_blob.metadata, big, src_blob.metadata.numel())
+                self._dma(dst_blob.metadata, src_blob.metadata, src_blob.metadata.numel())
                 if src_blob.offsets is not None:
-                    self._copy(dst_blob.offsets, src_blob.offsets, big, 8 * (src_blob.nblocks + 1))
+                    self._dma(dst_blob.offsets, src_blob.offsets, src_blob.nblocks + 1)
                     # payload length = offsets[nblocks], read on the device
                     self._copy(dst_blob.payload, src_blob.payload, src_blob.offsets[src_blob.nblocks:].data_ptr(),
                                src_blob.payload.numel())
                 else:  # codec none: static length
-                    self._copy(dst_blob.payload, src_blob.payload, big, src_blob.payload_nbytes())
+                    self._dma(dst_blob.payload, src_blob.payload, src_blob.payload_nbytes())
                 self.ev_copy[i].record(self.s_copy)
             dst_blob.nblocks = src_blob.nblocks
             dst_blob._nbytes = src_blob._nbytes
