@@ -73,7 +73,6 @@ class HostRoundTrip:
             self.s_in, self.s_enc, self.s_out, self.s_back, self.s_dec = mk(), mk(), mk(), mk(), mk()
             ev = lambda: [torch.cuda.Event() for _ in self.chunks]  # noqa: E731
             self.e_in, self.e_enc, self.e_out, self.e_back, self.e_dec = ev(), ev(), ev(), ev(), ev()
-            self._big = torch.full((1,), 1 << 62, dtype=torch.int64, device=self.device)
             torch.cuda.synchronize(self.device)
 
     def _copy(self, dst_ptr: int, src_ptr: int, len_ptr: int, max_bytes: int, stream) -> None:
@@ -86,8 +85,6 @@ class HostRoundTrip:
         into `out`; adds the squared reconstruction error to `err_sum`
         (device float64 scalar) if given.  Ordered before the device's
         current stream afterwards."""
-        lib = N.lib()
-        big = self._big.data_ptr()
         cur = torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
             for s in (self.s_in, self.s_enc, self.s_out, self.s_back, self.s_dec):
@@ -121,8 +118,10 @@ class HostRoundTrip:
                 if ho is not None:
                     self._copy(hp.data_ptr(), blob.payload.data_ptr(), blob.offsets[blob.nblocks:].data_ptr(),
                                hp.numel(), self.s_out)
-                else:
-                    self._copy(hp.data_ptr(), blob.payload.data_ptr(), big, blob.payload_nbytes(), self.s_out)
+                else:  # static length: the copy engine, no SMs taken from the codec
+                    n = blob.payload_nbytes()
+                    with torch.cuda.stream(self.s_out):
+                        hp[:n].copy_(blob.payload[:n], non_blocking=True)
                 self.e_out[i].record(self.s_out)
                 # host wire -> HBM (after the previous run's decode read rx)
                 self.s_back.wait_event(self.e_out[i])
@@ -137,7 +136,9 @@ class HostRoundTrip:
                     self._copy(rx.payload.data_ptr(), hp.data_ptr(), ho.data_ptr() + 8 * blob.nblocks, hp.numel(),
                                self.s_back)
                 else:
-                    self._copy(rx.payload.data_ptr(), hp.data_ptr(), big, blob.payload_nbytes(), self.s_back)
+                    n = blob.payload_nbytes()
+                    with torch.cuda.stream(self.s_back):
+                        rx.payload[:n].copy_(hp[:n], non_blocking=True)
                 self.e_back[i].record(self.s_back)
                 rx.nblocks, rx._nbytes = blob.nblocks, blob._nbytes
                 self.s_dec.wait_event(self.e_back[i])
