@@ -229,6 +229,19 @@ class KVCodec:
             bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
         if bt.numel() < need:
             raise ValueError(f"block_table has {bt.numel()} entries, {need} needed for {T} tokens")
+        # the fused kernels' paged-input conditions (fast128.cu paged_input_ok;
+        # the per-channel TMA kernel reads contiguous input only)
+        why = None
+        if self.encode_path.startswith("fast128"):
+            P = int(page_tokens)
+            tiles = P >= 4 and (64 % P == 0 if P < 64 else P % 64 == 0)
+            if not (self.in_dtype == torch.bfloat16 and T % 64 == 0 and tiles and layer_stride % (H * 128) == 0
+                    and pages.data_ptr() % 16 == 0):
+                why = "generic: paged input needs bf16, whole 64-token tiles and page runs that tile 64 tokens"
+        elif self.encode_path == "uchan128":
+            why = "generic: the per-channel kernel reads contiguous input"
+        if why:
+            _warn_generic(self.strategy_id, "paged encode", why)
         arr, cptr = self._classes_arg(head_classes)
         blob = out if out is not None else self.alloc_blob(arr)
         if arr is not None:
