@@ -316,6 +316,20 @@ __device__ __forceinline__ void quantize64(float* y, float mn0, float mx0, float
   }
 }
 
+// paged input (thread 0): the 64-token tile as one 5D box per page run; out
+// of line so the contiguous kernels' main loop is unchanged
+__device__ __noinline__ void issue_paged_tile(uint8_t* dst, const CUtensorMap* map, int64_t tile, int64_t T, int64_t H,
+                                              int64_t page_tokens, const int32_t* block_table, uint64_t* bar) {
+  const int64_t r0 = tile * kRows, lh = r0 / T, t0 = r0 - lh * T;
+  const int l = (int)(lh / H), h = (int)(lh - (int64_t)l * H);
+  const int bt = page_tokens < kRows ? (int)page_tokens : kRows;
+  for (int j = 0; j < kRows; j += bt) {
+    const int64_t t = t0 + j;
+    const int64_t prow = (int64_t)block_table[t / page_tokens] * page_tokens + t % page_tokens;
+    tma_load_5d(dst + j * 256, map, h, (int)prow, l, bar);
+  }
+}
+
 // ------------------------------------------------------------ encode kernel
 // W = compile-time symbol width (uniform strategies), 0 = per-row runtime width
 // F32: float32 input (the reference's own corpora): the tile is 64 rows x
@@ -334,9 +348,12 @@ __host__ __device__ constexpr int enc_smem_bytes() {
   return enc_stages<F32>() * enc_tile_bytes<F32>() + 1024 + 64;
 }
 
-template <int MODE, int G, int W, bool F32 = false>
+// PAGED: bf16 input read from a paged cache (5D boxes per page run); a
+// separate instantiation so the contiguous kernels keep their exact code
+template <int MODE, int G, int W, bool F32 = false, bool PAGED = false>
 __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
+  static_assert(!(F32 && PAGED), "paged input is bf16");
   constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -359,18 +376,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
   // tokens -- the same 128B-swizzled half rows, at 1 KB-aligned offsets
   auto issue = [&](int s, int64_t tile) {
     mbar_expect_tx(&full[s], TB);
-    if (F32 || !a.paged) {
+    if constexpr (PAGED)
+      issue_paged_tile(tiles + s * TB, &tmap, tile, g.T, g.H, a.page_tokens, a.block_table, &full[s]);
+    else
       tma_load_2d(tiles + s * TB, &tmap, 0, (int)(tile * kBoxRows), &full[s]);
-      return;
-    }
-    const int64_t r0 = tile * kRows, lh = r0 / g.T, t0 = r0 - lh * g.T;
-    const int l = (int)(lh / g.H), h = (int)(lh - (int64_t)l * g.H);
-    const int bt = a.page_tokens < kRows ? (int)a.page_tokens : kRows;
-    for (int j = 0; j < kRows; j += bt) {
-      const int64_t t = t0 + j;
-      const int64_t prow = (int64_t)a.block_table[t / a.page_tokens] * a.page_tokens + t % a.page_tokens;
-      tma_load_5d(tiles + s * TB + j * 256, &tmap, h, (int)prow, l, &full[s]);
-    }
   };
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       if (tid >= 2) {
         load_half(tb, tid - 2, pv);
       } else if (valid && t > 0) {
-        const int64_t prev = F32 ? (row - 1) * 128 + half * 64 : out_index(a, lh, t - 1, half * 64);
+        const int64_t prev = PAGED ? out_index(a, lh, t - 1, half * 64) : (row - 1) * 128 + half * 64;
         const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) +
                                                           prev * (F32 ? 4 : 2));
 #pragma unroll
@@ -1043,8 +1052,17 @@ bool make_input_map_f32(CUtensorMap* map, const void* kv, int64_t nrows) {
 template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   constexpr int smem = enc_smem_bytes<F32>();
-  auto k = k_enc128<MODE, G, W, F32>;
-  set_max_dyn_smem<k_enc128<MODE, G, W, F32>>(smem);
+  auto k = k_enc128<MODE, G, W, F32, false>;
+  if constexpr (!F32) {
+    if (a.paged) {
+      k = k_enc128<MODE, G, W, false, true>;
+      set_max_dyn_smem<k_enc128<MODE, G, W, false, true>>(smem);
+    } else {
+      set_max_dyn_smem<k_enc128<MODE, G, W, false, false>>(smem);
+    }
+  } else {
+    set_max_dyn_smem<k_enc128<MODE, G, W, F32, false>>(smem);
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
