@@ -223,6 +223,8 @@ class KVCodec:
         L, H, T, C = self.shape
         if page_tokens < 1 or layer_stride < 0:
             raise ValueError("page_tokens must be >= 1 and layer_stride >= 0")
+        if pages.numel() < L * layer_stride or layer_stride < page_tokens * H * C:
+            raise ValueError("page pool smaller than layers x layer_stride, or layer_stride below one page")
         need = -(-T // page_tokens)
         bt = block_table
         if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
@@ -289,6 +291,13 @@ class KVCodec:
         table (no host sync)."""
         if pages.dtype != self.out_dtype:
             raise ValueError("page dtype must match the plan's out_dtype")
+        L, H, T, C = self.shape
+        if page_tokens < 1 or layer_stride < page_tokens * H * C or pages.numel() < L * layer_stride:
+            raise ValueError("page pool smaller than layers x layer_stride, or layer_stride below one page")
+        if not pages.is_cuda or not pages.is_contiguous():
+            raise ValueError("pages must be a contiguous CUDA tensor")
+        if block_table.numel() < -(-T // page_tokens):
+            raise ValueError(f"block_table has {block_table.numel()} entries, {-(-T // page_tokens)} needed")
         if blob.metadata.numel() != self.metadata_bytes:
             raise N.CodecError(f"metadata is {blob.metadata.numel()} bytes, expected {self.metadata_bytes}")
         bt = block_table
