@@ -51,6 +51,12 @@ class DeviceBlob:
         L, H, T, C = self.shape
         return L * H * T * C * 2  # declared 16-bit source width (tensors.py:16, :69-72)
 
+    def refresh(self) -> None:
+        """Forget the cached payload length: call after a CUDA-graph replay
+        (or any encode enqueued outside encode()) re-filled this blob."""
+        if self.offsets is not None:
+            self._nbytes = None
+
     def payload_nbytes(self) -> int:
         """Payload length; syncs once for data-dependent codecs."""
         if self._nbytes is None:
