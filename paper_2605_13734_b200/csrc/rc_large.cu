@@ -26,7 +26,7 @@
 namespace kvc {
 namespace {
 
-constexpr int kLThreads = 128;
+constexpr int kLThreads = 224;  // 7 warps: two CTAs of 112 KB trees fill the SM (14 warps)
 
 // rows w = 5..8 of the reciprocal tables (rc_tables.cuh) in constant memory:
 // read with the warp-uniform position index through the constant cache, off
