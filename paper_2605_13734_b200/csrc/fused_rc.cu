@@ -448,7 +448,7 @@ __device__ __forceinline__ ChanMap chan_map(int64_t gt, int64_t nbt) {
   return r;
 }
 
-template <int W>
+template <int W, bool PAGED>
 __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedArgs a) {
   __shared__ __align__(16) uint8_t tiles[kFThreads / 32][32 * kTileStrideB];
   const Geo& g = a.g;
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
   // paged input: (l, token chunk, head, channel) order -- the warps in flight
   // cover every head of a token range (whole 2 KB rows of the page pool)
   int64_t gm = gt;
-  if (a.paged) {
+  if (PAGED) {
     const int64_t c = gt & 127, q = gt >> 7, h = q % g.H, q2 = q / g.H, tc = q2 % nbt, l = q2 / nbt;
     gm = ((l * g.H + h) * nbt + tc) * 128 + c;
   }
@@ -492,12 +492,12 @@ __global__ void __launch_bounds__(kFThreads, 8) k_fused_chan_encode(const FusedA
   uint64_t sacc = 0, zacc = 0;
 #pragma unroll 1
   for (int gi = 0; gi < ngr; ++gi) {
-    const uint4* rowp = a.paged ? paged_row(gi) : src + (int64_t)gi * 32 * 16;  // 32 tokens = 32 * 256 B
+    const uint4* rowp = PAGED ? paged_row(gi) : src + (int64_t)gi * 32 * 16;  // 32 tokens = 32 * 256 B
     uint4 v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __ldcs(rowp + k);  // read once (evict-first)
     if (gi + 1 < ngr) {
-      const uint4* nx = a.paged ? paged_row(gi + 1) : rowp + 32 * 16;
+      const uint4* nx = PAGED ? paged_row(gi + 1) : rowp + 32 * 16;
       prefetch_l1(nx);
       prefetch_l1(nx + 2);
     }
@@ -598,7 +598,11 @@ cudaError_t enc_w(const FusedArgs& a, cudaStream_t s) {
   if (g.uchan) {
     const int64_t nblocks = g.LH * 128 * (g.T / g.block);
     const int64_t threads = nblocks > a.max_blocks + 1 ? nblocks : a.max_blocks + 1;
-    k_fused_chan_encode<W><<<(unsigned)((threads + kFThreads - 1) / kFThreads), kFThreads, 0, s>>>(a);
+    const unsigned grid = (unsigned)((threads + kFThreads - 1) / kFThreads);
+    if (a.paged)
+      k_fused_chan_encode<W, true><<<grid, kFThreads, 0, s>>>(a);
+    else
+      k_fused_chan_encode<W, false><<<grid, kFThreads, 0, s>>>(a);
   } else {
     k_fused_tok_encode<W><<<(unsigned)((a.max_blocks + 1 + kFThreads - 1) / kFThreads), kFThreads, 0, s>>>(a);
   }
