@@ -24,7 +24,9 @@
  * caller and sized with the query functions; `head_classes` is a HOST array.
  * `stream` is a cudaStream_t (NULL = legacy default stream).  No call
  * allocates device memory; all device work is stream-ordered, and plans are
- * immutable after creation (safe to share across threads and streams).
+ * immutable after creation (safe to share across threads and streams).  A
+ * workspace carries one operation's scratch and status word: operations in
+ * flight at the same time (e.g. on two streams) need one workspace each.
  * Every function returns a kvc_status; on failure kvc_last_error() holds a
  * thread-local message.
  */
