@@ -105,7 +105,11 @@ def _warn_generic(sid: str, side: str, path: str) -> None:
 
 
 class KVCodec:
-    """A compiled plan (kvc_plan) plus its device workspace."""
+    """A compiled plan (kvc_plan) plus its device workspace.
+
+    The workspace holds one operation's scratch and status word: calls on
+    one KVCodec are ordered on their streams, and operations that must run
+    concurrently (K and V on two streams) use one KVCodec each."""
 
     def __init__(
         self,
