@@ -93,7 +93,7 @@ def test_config_scale_slab_parity(case):
     w, g = s.bits, s.group
     dev = torch.device("cuda", 0)
     free, _ = torch.cuda.mem_get_info(dev)
-    need = 2 * L * H * T * C * 2 * 1.4
+    need = 3 * L * H * T * C * 2 * 1.4  # kv, a decoded copy / the page pool, blobs
     if free < need:
         pytest.skip(f"needs {need / 1e9:.0f} GB of free HBM, {free / 1e9:.0f} GB available")
     kv, _ = synthetic_kv(L, H, T, C, seed=7, device=dev)
@@ -164,3 +164,25 @@ def test_config_scale_slab_parity(case):
         codec.check(decoding=True)
         view = pool.view(L, n_pages, pt, H, C)[:, table.long()].reshape(L, T, H, C).permute(0, 2, 1, 3)
         assert torch.equal(view, out), f"{case}: paged decode differs from the contiguous decode"
+        del pool, view
+
+    # the whole tensor encoded again straight from a paged cache
+    # (kvc_encode_paged, 16-token pages, random table): the same blob
+    del out
+    torch.cuda.empty_cache()
+    pt = 16
+    n_pages = T // pt
+    table = torch.randperm(n_pages, device=dev).to(torch.int32)
+    pool = torch.empty((L, n_pages * pt, H, C), dtype=torch.bfloat16, device=dev)
+    rows = (table.long()[:, None] * pt + torch.arange(pt, device=dev)[None, :]).reshape(-1)
+    for li in range(L):
+        pool[li, rows] = kv[li].permute(1, 0, 2)
+    blob2 = codec.encode_paged(pool, table, pt, n_pages * pt * H * C)
+    codec.check()
+    n = blob.payload_nbytes()
+    assert blob2.payload_nbytes() == n, f"{case}: paged encode payload length differs"
+    assert torch.equal(blob2.payload[:n], blob.payload[:n]), f"{case}: paged encode payload differs"
+    assert torch.equal(blob2.metadata, blob.metadata), f"{case}: paged encode metadata differs"
+    if blob.offsets is not None:
+        nb = blob.nblocks + 1
+        assert torch.equal(blob2.offsets[:nb], blob.offsets[:nb]), f"{case}: paged encode offsets differ"
