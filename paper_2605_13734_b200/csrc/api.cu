@@ -31,23 +31,82 @@ int cuda_fail(cudaError_t e, const char* what) {
 // ---------------------------------------------------------------- id parser
 // Grammar of strategy.py:8-19 (and the same validations: quantize.py:26-62,
 // transforms.py:25-30, codecs.py:32-38) plus the extension kinds.
-bool parse_int(const std::string& s, int& out) {
-  if (s.empty()) return false;
-  size_t i = (s[0] == '-' || s[0] == '+') ? 1 : 0;
-  if (i == s.size()) return false;
-  for (size_t k = i; k < s.size(); ++k)
-    if (s[k] < '0' || s[k] > '9') return false;
-  long v = strtol(s.c_str(), nullptr, 10);
-  if (v < -1000000 || v > 1000000) return false;
-  out = (int)v;
+// Python's int() / float() on a str (the reference parses with them,
+// strategy.py:68-109), for ASCII text: surrounding whitespace, a sign,
+// single underscores between digits, and for float a fraction, an exponent
+// or nan / inf / infinity in any case.  Hex and other strtod extensions are
+// rejected as Python rejects them.
+bool py_space(char c) { return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f); }
+
+std::string py_strip(const std::string& s) {
+  size_t a = 0, b = s.size();
+  while (a < b && py_space(s[a])) ++a;
+  while (b > a && py_space(s[b - 1])) --b;
+  return s.substr(a, b - a);
+}
+
+bool is_digit(char c) { return c >= '0' && c <= '9'; }
+
+// digits with single underscores between them, appended to `out` without
+// the underscores; false if no digit at i
+bool py_digits(const std::string& s, size_t& i, std::string& out) {
+  if (i >= s.size() || !is_digit(s[i])) return false;
+  while (i < s.size()) {
+    if (is_digit(s[i])) {
+      out += s[i++];
+    } else if (s[i] == '_' && i + 1 < s.size() && is_digit(s[i + 1])) {
+      ++i;
+    } else {
+      break;
+    }
+  }
   return true;
 }
 
-bool parse_double(const std::string& s, double& out) {
-  if (s.empty()) return false;
-  char* end = nullptr;
-  out = strtod(s.c_str(), &end);
-  return end && *end == '\0';
+bool parse_int(const std::string& raw, int& out) {
+  const std::string s = py_strip(raw);
+  size_t i = 0;
+  bool neg = false;
+  if (i < s.size() && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
+  std::string d;
+  if (!py_digits(s, i, d) || i != s.size()) return false;
+  size_t z = 0;
+  while (z + 1 < d.size() && d[z] == '0') ++z;
+  d = d.substr(z);
+  if (d.size() > 7) return false;  // far outside every valid width / group
+  const long v = strtol(d.c_str(), nullptr, 10);
+  out = (int)(neg ? -v : v);
+  return true;
+}
+
+bool parse_double(const std::string& raw, double& out) {
+  const std::string s = py_strip(raw);
+  size_t i = 0;
+  std::string num;
+  if (i < s.size() && (s[i] == '+' || s[i] == '-')) num += s[i++];
+  std::string rest = s.substr(i);
+  for (auto& c : rest) c = (char)tolower((unsigned char)c);
+  if (rest == "nan" || rest == "inf" || rest == "infinity") {
+    const double v = rest == "nan" ? NAN : INFINITY;
+    out = (!num.empty() && num[0] == '-') ? -v : v;
+    return true;
+  }
+  bool any = false;
+  if (i < s.size() && is_digit(s[i])) any = py_digits(s, i, num);
+  if (i < s.size() && s[i] == '.') {
+    num += s[i++];
+    if (i < s.size() && is_digit(s[i])) any = py_digits(s, i, num) || any;
+  }
+  if (!any) return false;
+  if (i < s.size() && (s[i] == 'e' || s[i] == 'E')) {
+    num += 'e';
+    ++i;
+    if (i < s.size() && (s[i] == '+' || s[i] == '-')) num += s[i++];
+    if (!py_digits(s, i, num)) return false;
+  }
+  if (i != s.size()) return false;
+  out = strtod(num.c_str(), nullptr);  // a plain decimal string: correctly rounded
+  return true;
 }
 
 std::string py_float_repr(double v) {
@@ -61,10 +120,7 @@ std::string py_float_repr(double v) {
   return s;
 }
 
-std::string trim(const std::string& s) {
-  size_t a = s.find_first_not_of(" \t\r\n\f\v"), b = s.find_last_not_of(" \t\r\n\f\v");
-  return a == std::string::npos ? std::string() : s.substr(a, b - a + 1);
-}
+std::string trim(const std::string& s) { return py_strip(s); }
 
 std::vector<std::string> split(const std::string& s, char c) {
   std::vector<std::string> out;
@@ -103,11 +159,19 @@ int parse_strategy(const char* text, Geo& g, double& rho, std::string& canon) {
   if (!kv(seg[1], k, v) || k != "q") return fail(KVC_ERR_CONFIG, "bad quant segment '" + seg[1] + "'");
   auto qt = split(v, ',');
   std::string kind = qt[0];
+  // a dict, as the reference builds it (strategy.py:84): a repeated key
+  // keeps its last value
   std::vector<std::pair<std::string, std::string>> params;
   for (size_t i = 1; i < qt.size(); ++i) {
     std::string a, b;
     if (!kv(qt[i], a, b)) return fail(KVC_ERR_CONFIG, "malformed token '" + qt[i] + "' in strategy id segment '" + seg[1] + "'");
-    params.push_back({a, b});
+    bool seen = false;
+    for (auto& p : params)
+      if (p.first == a) {
+        p.second = b;
+        seen = true;
+      }
+    if (!seen) params.push_back({a, b});
   }
   auto keys_are = [&](std::initializer_list<const char*> want) {
     if (params.size() != want.size()) return false;

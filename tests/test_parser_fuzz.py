@@ -1,0 +1,140 @@
+"""Differential fuzz of the strategy-id parsers (CPU): the C parser behind
+kvc_plan_create, the Python mirror (paper_2605_13734_b200.strategy), and --
+when /root/reference is mounted -- the reference's own parse_strategy_id
+(strategy.py:68-109) must accept and reject the same ids and agree on the
+canonical id.  Ids come from the grammar with mutated number tokens (Python
+int() / float() spellings: signs, spaces, underscores, exponents, nan / inf),
+dropped / duplicated / renamed parameters and stray separators."""
+
+import ctypes
+import os
+import sys
+
+import pytest
+
+hypothesis = pytest.importorskip("hypothesis")
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+from paper_2605_13734_b200 import _native as N  # noqa: E402
+from paper_2605_13734_b200.strategy import parse_strategy_id  # noqa: E402
+
+SHAPE = (1, 2, 1024, 128)
+REF = "/root/reference/pkg/src"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_13734_b200._build import build
+
+    build()
+    return N.lib()
+
+
+def _ref_parser():
+    if not os.path.isdir(REF):
+        return None
+    sys.path.insert(0, REF)
+    try:
+        from kvpilot.pipeline.strategy import parse_strategy_id as ref_parse  # type: ignore
+    except Exception:
+        return None
+    return ref_parse
+
+
+INTS = st.one_of(
+    st.sampled_from(["1", "2", "3", "4", "8", "16", "32", "64", "128", "0", "-1", "9", "256",
+                     " 4", "4 ", "+4", "04", "4_0", "1_6", "0x10", "4.0", "", "٤", "1e1", "32 "]),
+    st.integers(-3, 300).map(str),
+)
+FLOATS = st.one_of(
+    st.sampled_from(["0.25", "0.125", "0.5", "1", "0", "1.0", "0.0", ".5", "5.", "1e-1", "2.5e-1", "+0.25",
+                     " 0.25", "0.25 ", "nan", "inf", "-0.0", "1.5", "-0.1", "0_5", "0.2_5", "", "0.3000000000000000444"]),
+    st.floats(-0.5, 1.5, allow_nan=False).map(repr),
+)
+
+
+@st.composite
+def ids(draw):
+    t = draw(st.sampled_from(["identity", "delta", "hadamard", "affine", "fourier", "Identity", ""]))
+    c = draw(st.sampled_from(["none", "rle", "entropy", "zstd", " none", "entropy "]))
+    kind = draw(st.sampled_from(["uniform", "uchan", "mixed", "mixlayer", "mixtok", "vector"]))
+    if kind in ("uniform", "uchan", "vector"):
+        params = [("b", draw(INTS)), ("g", draw(INTS))]
+    else:
+        params = [("hi", draw(INTS)), ("lo", draw(INTS)), ("g", draw(INTS)), ("rho", draw(FLOATS))]
+    mut = draw(st.sampled_from(["none", "none", "none", "drop", "dup", "rename", "nokv", "order"]))
+    if mut == "drop" and params:
+        params.pop(draw(st.integers(0, len(params) - 1)))
+    elif mut == "dup":
+        params.append(params[0])
+    elif mut == "rename":
+        i = draw(st.integers(0, len(params) - 1))
+        params[i] = ("x", params[i][1])
+    elif mut == "order":
+        params = params[::-1]
+    toks = [f"{k}={v}" for k, v in params]
+    if mut == "nokv":
+        toks.append("b4")
+    q = ",".join([kind] + toks)
+    sid = f"t={t};q={q};c={c}"
+    sep = draw(st.sampled_from(["", "", "", ";", " ", "\n"]))
+    return sid + sep
+
+
+def _c_parse(lib, sid):
+    h = ctypes.c_void_p()
+    o = N.KvcOptions()
+    rc = lib.kvc_plan_create(ctypes.byref(h), sid.encode(), *SHAPE, ctypes.byref(o))
+    if rc != 0:
+        return rc, None
+    canon = lib.kvc_plan_strategy_id(h).decode()
+    lib.kvc_plan_destroy(h)
+    return rc, canon
+
+
+def _shape_ok(s):
+    q = s.quant
+    g = q.group_size
+    if q.kind == "uniform_channel":
+        return SHAPE[2] % g == 0 and g * SHAPE[3] * 5 <= 200 * 1024
+    return SHAPE[3] % g == 0
+
+
+@settings(max_examples=1500, deadline=None, derandomize=True)
+@given(ids())
+def test_parsers_agree(lib, sid):
+    try:
+        s = parse_strategy_id(sid)
+        py = s.id
+    except ValueError:
+        s, py = None, None
+    rc, canon = _c_parse(lib, sid)
+    if py is None:
+        assert rc != 0, (sid, canon)
+        return
+    if not _shape_ok(s):
+        assert rc != 0, (sid, "shape")
+        return
+    assert rc == 0, (sid, N.lib().kvc_last_error().decode())
+    assert canon == py, (sid, canon, py)
+
+
+@settings(max_examples=800, deadline=None, derandomize=True)
+@given(ids())
+def test_mirror_matches_reference_parser(sid):
+    ref = _ref_parser()
+    if ref is None:
+        pytest.skip("reference not mounted")
+    try:
+        want = ref(sid).id
+    except Exception:  # the reference raises ValueError (and its subclasses)
+        want = None
+    try:
+        got = parse_strategy_id(sid).id
+    except ValueError:
+        got = None
+    ext = any(k in sid for k in ("uchan", "mixlayer", "mixtok", "affine"))
+    if ext and want is None:
+        return  # extension kinds are absent from the reference grammar
+    assert got == want, (sid, got, want)
