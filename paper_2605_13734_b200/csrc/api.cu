@@ -32,17 +32,81 @@ int cuda_fail(cudaError_t e, const char* what) {
 // Grammar of strategy.py:8-19 (and the same validations: quantize.py:26-62,
 // transforms.py:25-30, codecs.py:32-38) plus the extension kinds.
 // Python's int() / float() on a str (the reference parses with them,
-// strategy.py:68-109), for ASCII text: surrounding whitespace, a sign,
-// single underscores between digits, and for float a fraction, an exponent
-// or nan / inf / infinity in any case.  Hex and other strtod extensions are
-// rejected as Python rejects them.
-bool py_space(char c) { return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f); }
+// strategy.py:68-109): surrounding whitespace, a sign, single underscores
+// between digits, any Unicode decimal digit (category Nd, Unicode 15.0 as in
+// CPython 3.12), and for float a fraction, an exponent or nan / inf /
+// infinity in any case.  Hex and other strtod extensions are rejected as
+// Python rejects them.  Ids arrive as UTF-8.
+bool utf8_decode(const std::string& s, std::vector<uint32_t>& cps, std::vector<size_t>* starts = nullptr) {
+  cps.clear();
+  for (size_t i = 0; i < s.size();) {
+    const unsigned char c = (unsigned char)s[i];
+    int n = c < 0x80 ? 1 : (c >> 5) == 0x6 ? 2 : (c >> 4) == 0xE ? 3 : (c >> 3) == 0x1E ? 4 : 0;
+    if (n == 0 || i + n > s.size()) return false;
+    uint32_t cp = n == 1 ? c : n == 2 ? (c & 0x1Fu) : n == 3 ? (c & 0x0Fu) : (c & 0x07u);
+    for (int k = 1; k < n; ++k) {
+      const unsigned char d = (unsigned char)s[i + k];
+      if ((d >> 6) != 0x2) return false;
+      cp = (cp << 6) | (d & 0x3Fu);
+    }
+    if (starts) starts->push_back(i);
+    cps.push_back(cp);
+    i += n;
+  }
+  if (starts) starts->push_back(s.size());
+  return true;
+}
 
-std::string py_strip(const std::string& s) {
-  size_t a = 0, b = s.size();
-  while (a < b && py_space(s[a])) ++a;
-  while (b > a && py_space(s[b - 1])) --b;
-  return s.substr(a, b - a);
+// str.isspace(); int() / float() strip the same set minus U+001C..U+001F
+bool py_isspace(uint32_t c) {
+  return (c >= 0x09 && c <= 0x0D) || (c >= 0x1C && c <= 0x20) || c == 0x85 || c == 0xA0 || c == 0x1680 ||
+         (c >= 0x2000 && c <= 0x200A) || c == 0x2028 || c == 0x2029 || c == 0x202F || c == 0x205F || c == 0x3000;
+}
+bool num_space(uint32_t c) { return py_isspace(c) && !(c >= 0x1C && c <= 0x1F); }
+
+// value of a Unicode decimal digit, or -1: the category-Nd zeros, each
+// followed by its nine digits
+int nd_digit(uint32_t c) {
+  static const uint32_t kZeros[] = {
+    0x30, 0x660, 0x6F0, 0x7C0, 0x966, 0x9E6, 0xA66, 0xAE6, 0xB66, 0xBE6,
+    0xC66, 0xCE6, 0xD66, 0xDE6, 0xE50, 0xED0, 0xF20, 0x1040, 0x1090, 0x17E0,
+    0x1810, 0x1946, 0x19D0, 0x1A80, 0x1A90, 0x1B50, 0x1BB0, 0x1C40, 0x1C50, 0xA620,
+    0xA8D0, 0xA900, 0xA9D0, 0xA9F0, 0xAA50, 0xABF0, 0xFF10, 0x104A0, 0x10D30, 0x11066,
+    0x110F0, 0x11136, 0x111D0, 0x112F0, 0x11450, 0x114D0, 0x11650, 0x116C0, 0x11730, 0x118E0,
+    0x11950, 0x11C50, 0x11D50, 0x11DA0, 0x11F50, 0x16A60, 0x16AC0, 0x16B50, 0x1D7CE, 0x1D7D8,
+    0x1D7E2, 0x1D7EC, 0x1D7F6, 0x1E140, 0x1E2F0, 0x1E4F0, 0x1E950, 0x1FBF0,
+  };
+  for (uint32_t z : kZeros)
+    if (c >= z && c < z + 10) return (int)(c - z);
+  return -1;
+}
+
+// a number token as Python sees it, in ASCII: number whitespace stripped,
+// decimal digits mapped to '0'..'9'; false if anything else is non-ASCII
+bool py_number_text(const std::string& raw, std::string& out) {
+  std::vector<uint32_t> cps;
+  if (!utf8_decode(raw, cps)) return false;
+  size_t a = 0, b = cps.size();
+  while (a < b && num_space(cps[a])) ++a;
+  while (b > a && num_space(cps[b - 1])) --b;
+  out.clear();
+  for (size_t i = a; i < b; ++i) {
+    const int d = nd_digit(cps[i]);
+    if (d >= 0) out += (char)('0' + d);
+    else if (cps[i] < 0x80) out += (char)cps[i];
+    else return false;
+  }
+  return true;
+}
+
+std::string py_strip(const std::string& s) {  // str.strip() on UTF-8 (unchanged if malformed)
+  std::vector<uint32_t> cps;
+  std::vector<size_t> at;
+  if (!utf8_decode(s, cps, &at)) return s;
+  size_t a = 0, b = cps.size();
+  while (a < b && py_isspace(cps[a])) ++a;
+  while (b > a && py_isspace(cps[b - 1])) --b;
+  return s.substr(at[a], at[b] - at[a]);
 }
 
 bool is_digit(char c) { return c >= '0' && c <= '9'; }
@@ -64,7 +128,8 @@ bool py_digits(const std::string& s, size_t& i, std::string& out) {
 }
 
 bool parse_int(const std::string& raw, int& out) {
-  const std::string s = py_strip(raw);
+  std::string s;
+  if (!py_number_text(raw, s)) return false;
   size_t i = 0;
   bool neg = false;
   if (i < s.size() && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
@@ -80,7 +145,8 @@ bool parse_int(const std::string& raw, int& out) {
 }
 
 bool parse_double(const std::string& raw, double& out) {
-  const std::string s = py_strip(raw);
+  std::string s;
+  if (!py_number_text(raw, s)) return false;
   size_t i = 0;
   std::string num;
   if (i < s.size() && (s[i] == '+' || s[i] == '-')) num += s[i++];

@@ -44,12 +44,14 @@ def _ref_parser():
 
 INTS = st.one_of(
     st.sampled_from(["1", "2", "3", "4", "8", "16", "32", "64", "128", "0", "-1", "9", "256",
-                     " 4", "4 ", "+4", "04", "4_0", "1_6", "0x10", "4.0", "", "٤", "1e1", "32 "]),
+                     " 4", "4 ", "+4", "04", "4_0", "1_6", "0x10", "4.0", "", "٤", "1e1", "32 ",
+                     "\u00a04", "4\u3000", "\x1c4", "\uff14", "\u0663\u0662", "\u0661_\u0662", "\u22124", "4__0"]),
     st.integers(-3, 300).map(str),
 )
 FLOATS = st.one_of(
     st.sampled_from(["0.25", "0.125", "0.5", "1", "0", "1.0", "0.0", ".5", "5.", "1e-1", "2.5e-1", "+0.25",
-                     " 0.25", "0.25 ", "nan", "inf", "-0.0", "1.5", "-0.1", "0_5", "0.2_5", "", "0.3000000000000000444"]),
+                     " 0.25", "0.25 ", "nan", "inf", "-0.0", "1.5", "-0.1", "0_5", "0.2_5", "", "0.3000000000000000444",
+                     "NaN", "-Infinity", "0x1p-2", "\u0660.\u0662\u0665", "2.5e\u0660-1", "0.25\u2028", "1e-1_0", "._5"]),
     st.floats(-0.5, 1.5, allow_nan=False).map(repr),
 )
 
@@ -78,7 +80,7 @@ def ids(draw):
         toks.append("b4")
     q = ",".join([kind] + toks)
     sid = f"t={t};q={q};c={c}"
-    sep = draw(st.sampled_from(["", "", "", ";", " ", "\n"]))
+    sep = draw(st.sampled_from(["", "", "", ";", " ", "\n", "\x1c", "\u3000", "\u00a0"]))
     return sid + sep
 
 
