@@ -458,16 +458,41 @@ def _checked_offsets(offsets, payload_len: int, nblocks: int) -> np.ndarray:
     return np.ascontiguousarray(o)
 
 
+def _whole_format_offsets(payload: np.ndarray, codec_kind: str, nblocks: int) -> np.ndarray:
+    """Block table of a reference whole-tensor payload (codecs.py:355-367),
+    which carries none: rle is one block; entropy is one BE32-length-prefixed
+    stream per width (codecs.py:364-366), walked here with the reference's
+    truncation / trailing-byte rules (codecs.py:412-413, :429-430)."""
+    n = payload.size
+    if codec_kind == "rle":
+        return np.array([0, n] if nblocks else [0], dtype=np.int64)
+    offs = [0]
+    for _ in range(nblocks):
+        o = offs[-1]
+        if o + 4 > n:
+            raise CodecError("entropy payload truncated at a stream header")
+        ln = int.from_bytes(payload[o:o + 4].tobytes(), "big")
+        if o + 4 + ln > n:
+            raise CodecError("entropy payload truncated inside a stream")
+        offs.append(o + 4 + ln)
+    if offs[-1] != n:
+        raise CodecError(f"{n - offs[-1]} trailing bytes in entropy payload")
+    return np.array(offs, dtype=np.int64)
+
+
 def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_symbols: int | None = 2048):
     """Full inverse pipeline on the GPU; returns (KVTensor fp32 on device, s_dec).
-    block_symbols=None: the blob is in the reference's whole-tensor format."""
+    block_symbols=None: the blob is in the reference's whole-tensor format --
+    including a CompressedBlob the reference's own compress() produced
+    (no block table, no device copy: both are derived here)."""
     s = as_strategy(s)
+    whole = block_symbols is None
     if block_symbols is None:
         block_symbols = reference_block_symbols(blob.shape)
     timer = timer if timer is not None else CudaEventTimer()
     _check_blob_matches(blob, s)
     dev = torch.device("cuda", torch.cuda.current_device())
-    dblob = blob.device
+    dblob = getattr(blob, "device", None)
     in_dtype = torch.bfloat16
     if dblob is None or dblob.payload.device != dev:
         codec = _plan(s.id, blob.shape, in_dtype, block_symbols)
@@ -480,14 +505,18 @@ def decompress(blob: CompressedBlob, s, timer: StageTimer | None = None, block_s
             raise CodecError("payload exceeds the plan's capacity")
         dblob.payload[: pay.size].copy_(torch.from_numpy(pay.copy()))
         dblob.metadata.copy_(torch.from_numpy(meta.copy()))
-        if blob.block_offsets is not None:
+        block_offsets = getattr(blob, "block_offsets", None)
+        if codec.codec_kind != "none":
             cls = (np.asarray(blob.bits_per_head) == s.quant.high_bits) if blob.mixed else None
-            offs_np = _checked_offsets(blob.block_offsets, pay.size, codec.num_blocks(head_classes=cls))
+            nblocks = codec.num_blocks(head_classes=cls)
+            if block_offsets is None:
+                if not whole:
+                    raise CodecError("rle/entropy blob without a block offset table")
+                block_offsets = _whole_format_offsets(pay, codec.codec_kind, nblocks)
+            offs_np = _checked_offsets(block_offsets, pay.size, nblocks)
             offs = torch.from_numpy(offs_np)
             dblob.offsets[: offs.numel()].copy_(offs)
             dblob.nblocks = offs.numel() - 1
-        elif codec.codec_kind != "none":
-            raise CodecError("rle/entropy blob without a block offset table")
         dblob._nbytes = pay.size
     else:
         codec = _plan(s.id, blob.shape, torch.bfloat16, block_symbols)

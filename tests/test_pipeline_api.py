@@ -200,3 +200,71 @@ def test_paged_decode_ragged_tokens(T, P):
         rows = (table.long()[:, None] * P + torch.arange(P, device="cuda")[None, :]).reshape(-1)[:T]
         got = pv[:, rows].permute(0, 2, 1, 3)
         assert torch.equal(got, flat), sid
+
+
+def _reference_blob(g, k, sid):
+    """A CompressedBlob as the reference's compress() builds it
+    (codecs.py:41-71): whole-tensor payload and metadata, no block table,
+    no device copy -- from the golden fixtures the unmodified reference wrote."""
+    from dataclasses import dataclass, field
+
+    from golden_io import items
+
+    @dataclass(frozen=True, eq=False)
+    class RefBlob:
+        payload: bytes
+        metadata: bytes
+        original_bytes: int
+        shape: tuple
+        group_size: int
+        bits_per_head: np.ndarray
+        mixed: bool
+        head_importance: np.ndarray = field(repr=False, default=None)
+
+    vals, imp = g["values"], g["importance"]
+    s = oracle.parse_id(sid)
+    L, H = vals.shape[:2]
+    if s.quant == "mixed":
+        cls = oracle.classify_heads(imp, s.rho)
+        bits = np.where(cls, s.hi, s.lo).astype(np.int64)
+    else:
+        bits = np.full((L, H), s.bits, dtype=np.int64)
+    pay = items(g["payload"], g["payload_off"])[k]
+    meta = items(g["metadata"], g["metadata_off"])[k]
+    return RefBlob(pay, meta, vals.size * 2, tuple(vals.shape), s.group, bits, s.quant == "mixed", imp)
+
+
+def test_decompress_consumes_reference_written_blobs():
+    """Drop-in in the other direction: blobs the reference CPU pipeline wrote
+    (all 180 ids, none / rle / entropy, mixed included) decompress on the GPU
+    to the reference's own reconstruction, bit for bit (block_symbols=None:
+    the whole-tensor format; the entropy block table is walked from the
+    BE32 stream headers)."""
+    from golden_io import load
+
+    from paper_2605_13734_b200 import decompress
+
+    g = load("pipeline_180.npz")
+    for k, sid in enumerate(g["ids"]):
+        sid = str(sid)
+        blob = _reference_blob(g, k, sid)
+        rec, _ = decompress(blob, sid, block_symbols=None)
+        got = rec.values.float().cpu().numpy() if hasattr(rec.values, "cpu") else np.asarray(rec.values)
+        assert np.array_equal(got.view(np.uint32), g["recon"][k].view(np.uint32)), sid
+
+
+def test_reference_written_blob_errors_are_codec_errors():
+    import dataclasses
+
+    from golden_io import load
+
+    from paper_2605_13734_b200 import CodecError, decompress
+
+    g = load("pipeline_180.npz")
+    ids = [str(x) for x in g["ids"]]
+    for sid in ("t=identity;q=uniform,b=2,g=32;c=entropy", "t=delta;q=mixed,hi=8,lo=2,g=32,rho=0.25;c=entropy",
+                "t=identity;q=uniform,b=4,g=64;c=rle"):
+        blob = _reference_blob(g, ids.index(sid), sid)
+        for bad in (blob.payload + b"\x00", blob.payload[:-1], blob.payload[:3]):
+            with pytest.raises(CodecError):
+                decompress(dataclasses.replace(blob, payload=bad), sid, block_symbols=None)
