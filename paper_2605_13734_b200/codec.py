@@ -239,6 +239,8 @@ class KVCodec:
         bt = block_table
         if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
             bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
+            if stream is not None:  # the converted copy must outlive the kernel on `stream`
+                bt.record_stream(stream)
         if bt.numel() < need:
             raise ValueError(f"block_table has {bt.numel()} entries, {need} needed for {T} tokens")
         # the fused kernels' paged-input conditions (fast128.cu paged_input_ok;
@@ -313,6 +315,8 @@ class KVCodec:
         bt = block_table
         if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
             bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
+            if stream is not None:  # the converted copy must outlive the kernel on `stream`
+                bt.record_stream(stream)
         nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
         N.check(
             self._lib.kvc_decode_paged(
