@@ -239,7 +239,8 @@ class KVCodec:
         bt = block_table
         if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
             bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
-            if stream is not None:  # the converted copy must outlive the kernel on `stream`
+            if stream is not None:  # the copy was made on the current stream: order and keep it
+                stream.wait_stream(torch.cuda.current_stream(self.device))
                 bt.record_stream(stream)
         if bt.numel() < need:
             raise ValueError(f"block_table has {bt.numel()} entries, {need} needed for {T} tokens")
@@ -315,7 +316,8 @@ class KVCodec:
         bt = block_table
         if bt.device != self.device or bt.dtype != torch.int32 or not bt.is_contiguous():
             bt = block_table.to(device=self.device, dtype=torch.int32).contiguous()
-            if stream is not None:  # the converted copy must outlive the kernel on `stream`
+            if stream is not None:  # the copy was made on the current stream: order and keep it
+                stream.wait_stream(torch.cuda.current_stream(self.device))
                 bt.record_stream(stream)
         nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
         N.check(
