@@ -27,8 +27,8 @@ def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def _stream_handle(stream: torch.cuda.Stream | None) -> int | None:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_handle(stream: torch.cuda.Stream | None, device: torch.device | None = None) -> int | None:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream or None
 
 
@@ -208,12 +208,13 @@ class KVCodec:
         blob = out if out is not None else self.alloc_blob(arr)
         if arr is not None:
             blob.head_classes = arr.astype(bool).reshape(self.shape[:2])
-        N.check(
-            self._lib.kvc_encode(
-                self._h, kv.data_ptr(), cptr, blob.payload.data_ptr(), blob.metadata.data_ptr() if self.metadata_bytes else blob.payload.data_ptr(),
-                _ptr(blob.offsets), self.workspace.data_ptr(), _stream_handle(stream),
+        with torch.cuda.device(self.device):
+            N.check(
+                self._lib.kvc_encode(
+                    self._h, kv.data_ptr(), cptr, blob.payload.data_ptr(), blob.metadata.data_ptr() if self.metadata_bytes else blob.payload.data_ptr(),
+                    _ptr(blob.offsets), self.workspace.data_ptr(), _stream_handle(stream, self.device),
+                )
             )
-        )
         if self.codec_kind == "none":
             blob._nbytes = int(self._lib.kvc_static_payload_bytes(self._h, cptr))
             blob.nblocks = 0
@@ -261,13 +262,14 @@ class KVCodec:
         blob = out if out is not None else self.alloc_blob(arr)
         if arr is not None:
             blob.head_classes = arr.astype(bool).reshape(self.shape[:2])
-        N.check(
-            self._lib.kvc_encode_paged(
-                self._h, pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), cptr,
-                blob.payload.data_ptr(), blob.metadata.data_ptr() if self.metadata_bytes else blob.payload.data_ptr(),
-                _ptr(blob.offsets), self.workspace.data_ptr(), _stream_handle(stream),
+        with torch.cuda.device(self.device):
+            N.check(
+                self._lib.kvc_encode_paged(
+                    self._h, pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), cptr,
+                    blob.payload.data_ptr(), blob.metadata.data_ptr() if self.metadata_bytes else blob.payload.data_ptr(),
+                    _ptr(blob.offsets), self.workspace.data_ptr(), _stream_handle(stream, self.device),
+                )
             )
-        )
         if self.codec_kind == "none":
             blob._nbytes = int(self._lib.kvc_static_payload_bytes(self._h, cptr))
             blob.nblocks = 0
@@ -288,12 +290,13 @@ class KVCodec:
         if blob.metadata.numel() != self.metadata_bytes:
             raise N.CodecError(f"metadata is {blob.metadata.numel()} bytes, expected {self.metadata_bytes}")
         nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
-        N.check(
-            self._lib.kvc_decode(
-                self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),
-                out.data_ptr(), self.workspace.data_ptr(), _stream_handle(stream),
+        with torch.cuda.device(self.device):
+            N.check(
+                self._lib.kvc_decode(
+                    self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),
+                    out.data_ptr(), self.workspace.data_ptr(), _stream_handle(stream, self.device),
+                )
             )
-        )
         return out
 
     def decode_paged(self, blob: DeviceBlob, pages: torch.Tensor, block_table: torch.Tensor, page_tokens: int,
@@ -320,18 +323,20 @@ class KVCodec:
                 stream.wait_stream(torch.cuda.current_stream(self.device))
                 bt.record_stream(stream)
         nbytes = -1 if (device_length and blob.offsets is not None) else blob.payload_nbytes()
-        N.check(
-            self._lib.kvc_decode_paged(
-                self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),
-                pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), self.workspace.data_ptr(),
-                _stream_handle(stream),
+        with torch.cuda.device(self.device):
+            N.check(
+                self._lib.kvc_decode_paged(
+                    self._h, blob.payload.data_ptr(), nbytes, blob.metadata.data_ptr(), _ptr(blob.offsets),
+                    pages.data_ptr(), bt.data_ptr(), int(page_tokens), int(layer_stride), self.workspace.data_ptr(),
+                    _stream_handle(stream, self.device),
+                )
             )
-        )
         return pages
 
     def check(self, stream: torch.cuda.Stream | None = None, decoding: bool = False) -> int:
         """Synchronise and raise ValueError / CodecError for device-side errors."""
         flags = ctypes.c_uint32(0)
-        N.check(self._lib.kvc_read_status(self._h, self.workspace.data_ptr(), _stream_handle(stream), ctypes.byref(flags)))
+        with torch.cuda.device(self.device):
+            N.check(self._lib.kvc_read_status(self._h, self.workspace.data_ptr(), _stream_handle(stream, self.device), ctypes.byref(flags)))
         N.raise_for_flags(int(flags.value), decoding)
         return int(flags.value)

@@ -104,3 +104,23 @@ def test_two_gpus_paged_connector():
     tx.check()
     torch.cuda.synchronize(1)
     assert torch.equal(dst[:, drows].permute(0, 2, 1, 3).cpu(), want)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_codec_on_another_device_than_current():
+    """A KVCodec on cuda:1 used while cuda:0 is the current device: its calls
+    run on its own device and stream, and give cuda:0's results."""
+    from paper_2605_13734_b200 import KVCodec
+
+    shape = (2, 4, 512, 128)
+    kv0 = _kv(shape, 12).cuda(0)
+    for sid in ("t=hadamard;q=uniform,b=4,g=32;c=none", "t=identity;q=uniform,b=2,g=32;c=entropy"):
+        c0 = KVCodec(sid, shape, device="cuda:0")
+        c1 = KVCodec(sid, shape, device="cuda:1")
+        torch.cuda.set_device(0)
+        want = c0.decode(c0.encode(kv0)).cpu()
+        kv1 = kv0.to("cuda:1")
+        b1 = c1.encode(kv1)
+        got = c1.decode(b1)
+        c1.check(decoding=True)
+        assert got.device.index == 1 and torch.equal(got.cpu(), want), sid
