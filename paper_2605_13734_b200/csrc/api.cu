@@ -403,12 +403,13 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
     p.ws_delta = off;
     off = align_up(off + delta128_ws_bytes(g), 256);
   }
-  // fused Hadamard encode: list of rows for the exact fixup pass (one int32
-  // per token row at most, plus the count)
+  // fused Hadamard encode: two row lists (one int32 per token row at most
+  // each, counts in a shared 16-byte header): rows the certified float32
+  // pass hands to the float64 pass, and rows left to the exact fixup pass
   p.ws_fix = -1;
   if (g.transform == T_HADAMARD && fast128_applicable(g)) {
     p.ws_fix = off;
-    off = align_up(off + 16 + 4 * g.LH * g.T, 256);
+    off = align_up(off + 16 + 8 * g.LH * g.T, 256);
   }
   p.ws_bytes = off;
   snprintf(p.id, sizeof p.id, "%s", canon.c_str());
@@ -504,6 +505,10 @@ static void fill_common(const Plan& p, double& hk, double& hc) {
   hc = std::sqrt((double)p.g.C);
   hk = std::ldexp(1.0 / hc, 896);
 }
+static void fill_common_enc(const Plan& p, double& hk, double& hc, float& hr32) {
+  fill_common(p, hk, hc);
+  hr32 = (float)(1.0 / hc);
+}
 
 static int encode_impl(const kvc_plan* plan, const void* kv, int paged, const int32_t* block_table,
                        int64_t page_tokens, int64_t layer_stride, const uint8_t* head_classes, void* payload,
@@ -582,7 +587,7 @@ static int encode_impl(const kvc_plan* plan, const void* kv, int paged, const in
   a.heads = heads;
   a.st = st;
   a.status = status;
-  fill_common(p, a.hk, a.hc);
+  fill_common_enc(p, a.hk, a.hc, a.hr32);
   for (int w = 1; w <= 8; ++w) a.rl[w] = 1.0f / (float)((1 << w) - 1);
   const bool aligned = g.uchan ? (g.T % 8 == 0) : (g.C % 8 == 0);
   if (!aligned) {
@@ -593,7 +598,13 @@ static int encode_impl(const kvc_plan* plan, const void* kv, int paged, const in
   if (fix) {
     a.fix_count = reinterpret_cast<uint32_t*>(ws + p.ws_fix);
     a.fix_rows = reinterpret_cast<int32_t*>(ws + p.ws_fix + 16);
-    if ((e = cudaMemsetAsync(a.fix_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e, "memset");
+    // KVC_HADAMARD_FP64=1 keeps every row on the float64 encoder (A/B runs)
+    static const bool fp64_only = getenv("KVC_HADAMARD_FP64") && atoi(getenv("KVC_HADAMARD_FP64")) != 0;
+    if (!fp64_only) {
+      a.fix1_count = a.fix_count + 1;
+      a.fix1_rows = a.fix_rows + g.LH * g.T;
+    }
+    if ((e = cudaMemsetAsync(a.fix_count, 0, 8, s)) != cudaSuccess) return cuda_fail(e, "memset");
   }
   if (fast128_applicable(g))
     e = launch_encode_fast128(a, p.sm_count, s);

@@ -330,6 +330,300 @@ __device__ __noinline__ void issue_paged_tile(uint8_t* dst, const CUtensorMap* m
   }
 }
 
+// float32 bit pattern of local value i: w[] holds 32 bf16 pairs or 64 fp32
+// bit patterns of this thread's half row
+template <bool F32>
+__device__ __forceinline__ uint32_t vbits_of(const uint32_t* w, int i) {
+  if constexpr (F32) return w[i];
+  return (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
+}
+
+// Hadamard of one row held by a thread pair (this thread: channels
+// 64*half..+63 in wv), float64 butterfly in the reference's stage order
+// (transforms.py:41-46), then RN32(RN64(S / sqrt 128)).  Leaves this thread's
+// 64 outputs in y (chunk 0: channels 32*half.., chunk 1: 64 + 32*half..) and
+// returns true when the row must be re-encoded exactly (k_encode_fixup).
+template <bool F32>
+__device__ __forceinline__ bool had64_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc) {
+  // Input range of the whole row (this half and the partner's): with every
+  // |x| in [2^-100, 2^101) no Hadamard output can overflow f32 or be a
+  // nonzero f32 subnormal, so the rounding below needs only the
+  // near-midpoint test.  NaN / inf inputs (which the 2^-896
+  // reinterpretation would turn into finite doubles) show up here too
+  // (tensors.py:41-42).  Zeros, extreme magnitudes and near-midpoint
+  // results send the row to the exact fixup pass (k_encode_fixup).
+  bool row_ok;
+  if constexpr (F32) {  // |x| as unsigned bit patterns order like the floats
+    uint32_t amx = wv[0] & 0x7FFFFFFFu, amn = amx;
+#pragma unroll
+    for (int k = 1; k < 64; ++k) {
+      const uint32_t aw = wv[k] & 0x7FFFFFFFu;
+      amx = max(amx, aw);
+      amn = min(amn, aw);
+    }
+    if (amx >= 0x7F800000u) nanacc = 1.0f;
+    amx = max(amx, (uint32_t)__shfl_xor_sync(0xffffffffu, amx, 1));
+    amn = min(amn, (uint32_t)__shfl_xor_sync(0xffffffffu, amn, 1));
+    const uint32_t emax = (amx >> 23) & 0xFFu, emin = (amn >> 23) & 0xFFu;
+    row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+  } else {
+    uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
+#pragma unroll
+    for (int k = 1; k < 32; ++k) {
+      const uint32_t aw = wv[k] & 0x7FFF7FFFu;
+      amx = bmax2(amx, aw);
+      amn = bmin2(amn, aw);
+    }
+    amx = bmax2(amx, __byte_perm(amx, 0, 0x1032));
+    amn = bmin2(amn, __byte_perm(amn, 0, 0x1032));
+    if ((amx & 0x7F80u) == 0x7F80u) nanacc = 1.0f;
+    amx = bmax2(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
+    amn = bmin2(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
+    const uint32_t emax = (amx >> 7) & 0xFFu, emin = (amn >> 7) & 0xFFu;
+    row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+  }
+  double f[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) f[i] = f32bits_scaled_f64(vbits_of<F32>(wv, i));
+  // stages h = 1..32 (transforms.py:41-46 order), in registers.  At h = 32
+  // thread B (half 1) writes its two outputs swapped (u - v at i, u + v at
+  // i + 32; the same roundings, as one DFMA with -1 each), so afterwards
+  // both threads hold the value the partner needs at local 32 + k and the
+  // one they keep at local k: the h = 64 exchange below needs no selects.
+  const double sgn = half ? -1.0 : 1.0;
+#pragma unroll
+  for (int h = 1; h < 64; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if ((i & h) == 0) {
+        const double u = f[i], v = f[i + h];
+        if (h == 32) {
+          f[i] = __fma_rn(v, sgn, u);
+          f[i + h] = __fma_rn(v, -sgn, u);
+        } else {
+          f[i] = u + v;
+          f[i + h] = u - v;
+        }
+      }
+    }
+  }
+  // stage h = 64 across the thread pair: A (half 0) keeps outputs 0..31 and
+  // 64..95, B keeps 32..63 and 96..127.  A's local k / 32 + k hold its
+  // T[k] / T[32 + k]; B's hold T[32 + k] / T[k].  Each sends local 32 + k
+  // and forms (own + r, own - r): A gets out[k], out[64 + k]; B gets
+  // out[32 + k] (a + b = b + a) and -out[96 + k] (own - r = -(r - own),
+  // negated back through the sign of the scale below).
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double send = f[32 + k];
+    const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(send), 1);
+    const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(send), 1);
+    const double r = __hiloint2double(hi, lo);
+    const double u = f[k];
+    f[k] = u + r;
+    f[32 + k] = u - r;
+  }
+  // RN32(RN64(S / sqrt n)) as one F2F of RN64(S * RN64(1/sqrt n)); the two
+  // differ only within 4 ulp64 of an f32 rounding midpoint (numerics.cuh).
+  // B's second half is scaled by -hk (RN is sign-symmetric; an exact zero
+  // comes out as -0 there, made +0 in the group min / max below).
+  const double hk2 = half ? -a.hk : a.hk;
+  bool mid = false;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const double q = f[i] * (i < 32 ? a.hk : hk2);
+    mid |= ((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x0FFFFFFCu <= 8u;
+    y[i] = __double2float_rn(q);
+  }
+  bool need_fix = !row_ok || mid;
+  need_fix |= __shfl_xor_sync(0xffffffffu, (int)need_fix, 1) != 0;
+  return need_fix;
+}
+
+// ---------------------------------------------------------------------------
+// Certified float32 Hadamard encode (bf16 input, 32-channel groups: the
+// reference default profile, transforms.py:62 + quantize.py:142-154).
+//
+// The reference's y = RN32(RN64(S / c)) (S the float64 butterfly sum,
+// c = RN64(sqrt 128)) reaches the payload only through three decisions, each
+// monotone in y: the fp16 zero RN16(min y), the fp16 scale
+// RN16(RN64(RN32(max y - min y) / levels)) and each symbol
+// clip(rint(RN32(RN32(y - z) / s))).  So the butterfly runs in float32 (two
+// values per FADD2) with a rigorous bound |y_hat - y| <= D on every output:
+//   D = ((7 - kex) + 3.01) u Sum|x| / c + 2^-140,        u = 2^-24.
+// bf16 inputs are multiples of 2^(emin-7) below 2^(emax+1), so the partial
+// sums of the first kex = clamp(16 - (emax - emin), 0, 7) stages fit 24 bits
+// and are exact (in any stage order); the other 7 - kex stages add at most
+// gamma_(7-kex) Sum|x| (summation tree of that depth), the scaling by
+// RN32(1/c) 2u Sum|x| / c, the reference's own roundings u Sum|x| / c, and
+// subnormal intermediates below 2^-146 in all.  A group is certified when
+// every decision is constant on [y_hat - D, y_hat + D]: the zero and the
+// scale are evaluated at both ends of their intervals (directed rounding),
+// and every quotient must lie farther than tau = D / s + 2^-20 (|t| + 1)
+// from its rounding boundary.  A certified row's bytes equal the reference's;
+// a row with an uncertified group goes to the float64 pass (k_had64_list, the
+// reference's butterfly in stage order), and rows with non-finite or huge
+// inputs straight to the exact fixup pass (k_encode_fixup).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// min / max of 32 floats, two new values per FMNMX3
+__device__ __forceinline__ void minmax32_3(const float* y, float& mn, float& mx) {
+  mn = fminf(y[0], y[1]);
+  mx = fmaxf(y[0], y[1]);
+#pragma unroll
+  for (int i = 2; i < 32; i += 2) {
+    mn = min3f(mn, y[i], y[i + 1]);
+    mx = max3f(mx, y[i], y[i + 1]);
+  }
+}
+__device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushort(__float2half_rn(v)); }
+
+// Float32 Hadamard of the row held by a thread pair (this thread: channels
+// 64*half..+63 as bf16 pairs in wv).  y gets this thread's 64 outputs
+// (chunk 0: channels 32*half.., chunk 1: 64 + 32*half.., the same layout as
+// had64_row; B's chunk 1 as -(-y), an exact zero there as -0); returns D.
+// row_ok: no non-finite input and every |x| < 2^101 (no float32 overflow).
+__device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc,
+                                           bool& row_ok) {
+  int kex;
+  {
+    uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
+#pragma unroll
+    for (int k = 1; k < 32; ++k) {
+      const uint32_t aw = wv[k] & 0x7FFF7FFFu;
+      amx = bmax2(amx, aw);
+      amn = bmin2(amn, aw);
+    }
+    amx = bmax2(amx, __byte_perm(amx, 0, 0x1032));
+    amn = bmin2(amn, __byte_perm(amn, 0, 0x1032));
+    if ((amx & 0x7F80u) == 0x7F80u) nanacc = 1.0f;
+    amx = bmax2(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
+    amn = bmin2(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
+    const int emax = (int)((amx >> 7) & 0xFFu), emin = (int)((amn >> 7) & 0xFFu);
+    row_ok = emax <= 127 + 100;
+    kex = min(max(16 - (emax - emin), 0), 7);
+  }
+  // P[m] = (local m, local m + 32): stages h = 1..16 pair P[m] with P[m + h]
+  float2 P[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m)
+    P[m] = make_float2(__uint_as_float(vbits_of<false>(wv, m)), __uint_as_float(vbits_of<false>(wv, m + 32)));
+  // h = 1, and Sum|x| as max(|a + b|, |a - b|) = |a| + |b| per pair
+  float2 sa = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int m = 0; m < 32; m += 2) {
+    const float2 s = f2add(P[m], P[m + 1]), d = f2sub(P[m], P[m + 1]);
+    sa = f2add(sa, make_float2(fmaxf(fabsf(s.x), fabsf(d.x)), fmaxf(fabsf(s.y), fabsf(d.y))));
+    P[m] = s;
+    P[m + 1] = d;
+  }
+#pragma unroll
+  for (int h = 2; h < 32; h <<= 1) {
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if ((m & h) == 0) {
+        const float2 s = f2add(P[m], P[m + h]), d = f2sub(P[m], P[m + h]);
+        P[m] = s;
+        P[m + h] = d;
+      }
+    }
+  }
+  // h = 32 inside each pair; thread B keeps local 32 + m and sends local m
+  // (one FFMA by -+1 each, the same roundings), as had64_row
+  const float sg = half ? -1.0f : 1.0f;
+  float K[32], Y[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    K[m] = __fmaf_rn(P[m].y, sg, P[m].x);
+    Y[m] = __fmaf_rn(P[m].y, -sg, P[m].x);
+  }
+  // h = 64 across the pair, then the scaling by RN32(1/c) (-RN32(1/c) for
+  // B's negated chunk 1)
+  const float2 r2 = make_float2(a.hr32, a.hr32);
+  const float2 n2 = half ? make_float2(-a.hr32, -a.hr32) : r2;
+#pragma unroll
+  for (int m = 0; m < 32; m += 2) {
+    const float2 rv = make_float2(__shfl_xor_sync(0xffffffffu, Y[m], 1), __shfl_xor_sync(0xffffffffu, Y[m + 1], 1));
+    const float2 kv = make_float2(K[m], K[m + 1]);
+    const float2 s = f2mul(f2add(kv, rv), r2), d = f2mul(f2sub(kv, rv), n2);
+    y[m] = s.x;
+    y[m + 1] = s.y;
+    y[32 + m] = d.x;
+    y[33 + m] = d.y;
+  }
+  float s1 = sa.x + sa.y;
+  s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+  // (10.01 - kex) u / c, rounded up generously (1.002 covers the float32
+  // evaluation of Sum|x| and of this coefficient)
+  const float coef = (10.01f - (float)kex) * 0x1p-24f * a.hr32 * 1.002f;
+  return __fmaf_ru(s1, coef, 0x1p-140f);
+}
+
+// Quantize one certified group of 32 values (yy -> magic floats 2^23 + 1.5
+// 2^23 + symbol, as quantize64) with fp16 scale / zero s16 / z16; returns
+// false when a decision is not constant over +-D (the row is then re-encoded
+// by the float64 pass, which also rewrites s16 / z16).
+__device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float D, int w, float rl,
+                                           unsigned short& s16, unsigned short& z16) {
+  const float lv = (float)((1 << w) - 1);
+  // zero RN16(min y), min y in [mn - D, mn + D]
+  const unsigned short zl = rn16(__fsub_rd(mn, D)), zh = rn16(__fadd_ru(mn, D));
+  // scale RN16(RN64(RN32(max - min) / lv)), RN32(max - min) in [dl, dh]
+  const float dl = __fsub_rd(__fsub_rd(mx, mn), 2.0f * D), dh = __fadd_ru(__fsub_ru(mx, mn), 2.0f * D);
+  const unsigned short sl = rn16(__fmul_rn(__fmul_rn(dl, rl), 0.99999904632568359375f));
+  const unsigned short sh = rn16(__fmul_rn(__fmul_rn(dh, rl), 1.00000095367431640625f));
+  s16 = sl;
+  z16 = zl;
+  const float s = __half2float(__ushort_as_half(sl)), z = __half2float(__ushort_as_half(zl));
+  bool ok = zl == zh && sl == sh && dl > 0.0f && !isinf(s) && !isinf(z);
+  // s == 0: r = 0 turns every quotient into 0 (symbol 0, quantize.py:154)
+  const float r = s > 0.0f ? __frcp_rn(s) : 0.0f;
+  const float dlo = __fsub_rn(mn, z), dhi = __fsub_rn(mx, z);
+  const float l0 = __fmul_rn(dlo, r), h0 = __fmul_rn(dhi, r);
+  const float l1 = __fmaf_rn(__fmaf_rn(-l0, s, dlo), r, l0);
+  const float h1 = __fmaf_rn(__fmaf_rn(-h0, s, dhi), r, h0);
+  const float tau = __fmaf_ru(D, r * 1.0001f, 0x1p-20f * (fmaxf(fabsf(l1), fabsf(h1)) + 1.0f));
+  const bool easy = l1 >= -0.5f && h1 < lv + 0.5f;
+  float racc = 0.0f;
+  float2* y2 = reinterpret_cast<float2*>(yy);
+  const float2 nz = f2(-z, -z), rr = f2(r, r), ns = f2(-s, -s), mg = f2(kMagicRound, kMagicRound);
+  const float2 nmg = f2(-kMagicRound, -kMagicRound);
+  if (__all_sync(0xffffffffu, easy)) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 d = f2add(y2[i], nz);
+      const float2 q0 = f2mul(d, rr);
+      const float2 q1 = f2fma(f2fma(q0, ns, d), rr, q0);
+      const float2 m = f2add(q1, mg);
+      const float2 rho = f2sub(q1, f2add(m, nmg));
+      racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
+      y2[i] = m;
+    }
+  } else {
+    const float top = kMagicRound + lv;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 d = f2add(y2[i], nz);
+      const float2 q0 = f2mul(d, rr);
+      const float2 q1 = f2fma(f2fma(q0, ns, d), rr, q0);
+      const float2 m = f2add(q1, mg);
+      const float2 rho = f2sub(q1, f2add(m, nmg));
+      racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
+      y2[i] = f2(fminf(fmaxf(m.x, kMagicRound), top), fminf(fmaxf(m.y, kMagicRound), top));
+    }
+  }
+  return ok && racc < 0.5f - tau;
+}
+
 // ------------------------------------------------------------ encode kernel
 // W = compile-time symbol width (uniform strategies), 0 = per-row runtime width
 // F32: float32 input (the reference's own corpora): the tile is 64 rows x
@@ -350,10 +644,13 @@ __host__ __device__ constexpr int enc_smem_bytes() {
 
 // PAGED: bf16 input read from a paged cache (5D boxes per page run); a
 // separate instantiation so the contiguous kernels keep their exact code
-template <int MODE, int G, int W, bool F32 = false, bool PAGED = false>
-__global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DELTA) ? 3 : 4)
+// CERT: the certified float32 Hadamard (bf16, G = 32) with the float64 pass
+// behind it for the rows it cannot certify
+template <int MODE, int G, int W, bool F32 = false, bool PAGED = false, bool CERT = false>
+__global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   static_assert(!(F32 && PAGED), "paged input is bf16");
+  static_assert(!CERT || (MODE == M_HADAMARD && !F32 && G == 32), "certified path: bf16 Hadamard, 32-channel groups");
   constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -453,101 +750,16 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
     int cb0, cb1;
     bool hadlayout = false;
     bool need_fix = false;  // Hadamard: this row is re-encoded exactly by k_encode_fixup
+    bool row_ok = true;     // certified path: finite inputs below 2^101
+    float Dcert = 0.0f;     // certified path: error bound of the float32 outputs
     const uint32_t flags_before = flags;
     if (MODE == M_HADAMARD) {
-      // Input range of the whole row (this half and the partner's): with every
-      // |x| in [2^-100, 2^101) no Hadamard output can overflow f32 or be a
-      // nonzero f32 subnormal, so the rounding below needs only the
-      // near-midpoint test.  NaN / inf inputs (which the 2^-896
-      // reinterpretation would turn into finite doubles) show up here too
-      // (tensors.py:41-42).  Zeros, extreme magnitudes and near-midpoint
-      // results send the row to the exact fixup pass (k_encode_fixup).
-      bool row_ok;
-      if constexpr (F32) {  // |x| as unsigned bit patterns order like the floats
-        uint32_t amx = wv[0] & 0x7FFFFFFFu, amn = amx;
-#pragma unroll
-        for (int k = 1; k < 64; ++k) {
-          const uint32_t aw = wv[k] & 0x7FFFFFFFu;
-          amx = max(amx, aw);
-          amn = min(amn, aw);
-        }
-        if (amx >= 0x7F800000u) nanacc = 1.0f;
-        amx = max(amx, (uint32_t)__shfl_xor_sync(0xffffffffu, amx, 1));
-        amn = min(amn, (uint32_t)__shfl_xor_sync(0xffffffffu, amn, 1));
-        const uint32_t emax = (amx >> 23) & 0xFFu, emin = (amn >> 23) & 0xFFu;
-        row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+      if constexpr (CERT) {
+        Dcert = had32_row(wv, half, a, y, nanacc, row_ok);
       } else {
-        uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
-#pragma unroll
-        for (int k = 1; k < 32; ++k) {
-          const uint32_t aw = wv[k] & 0x7FFF7FFFu;
-          amx = bmax2(amx, aw);
-          amn = bmin2(amn, aw);
-        }
-        amx = bmax2(amx, __byte_perm(amx, 0, 0x1032));
-        amn = bmin2(amn, __byte_perm(amn, 0, 0x1032));
-        if ((amx & 0x7F80u) == 0x7F80u) nanacc = 1.0f;
-        amx = bmax2(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
-        amn = bmin2(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
-        const uint32_t emax = (amx >> 7) & 0xFFu, emin = (amn >> 7) & 0xFFu;
-        row_ok = emax <= 127u + 100u && emin >= 127u - 100u;
+        need_fix = had64_row<F32>(wv, half, a, y, nanacc);
+        if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       }
-      double f[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) f[i] = f32bits_scaled_f64(vbits(wv, i));
-      // stages h = 1..32 (transforms.py:41-46 order), in registers.  At h = 32
-      // thread B (half 1) writes its two outputs swapped (u - v at i, u + v at
-      // i + 32; the same roundings, as one DFMA with -1 each), so afterwards
-      // both threads hold the value the partner needs at local 32 + k and the
-      // one they keep at local k: the h = 64 exchange below needs no selects.
-      const double sgn = half ? -1.0 : 1.0;
-#pragma unroll
-      for (int h = 1; h < 64; h <<= 1) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          if ((i & h) == 0) {
-            const double u = f[i], v = f[i + h];
-            if (h == 32) {
-              f[i] = __fma_rn(v, sgn, u);
-              f[i + h] = __fma_rn(v, -sgn, u);
-            } else {
-              f[i] = u + v;
-              f[i + h] = u - v;
-            }
-          }
-        }
-      }
-      // stage h = 64 across the thread pair: A (half 0) keeps outputs 0..31 and
-      // 64..95, B keeps 32..63 and 96..127.  A's local k / 32 + k hold its
-      // T[k] / T[32 + k]; B's hold T[32 + k] / T[k].  Each sends local 32 + k
-      // and forms (own + r, own - r): A gets out[k], out[64 + k]; B gets
-      // out[32 + k] (a + b = b + a) and -out[96 + k] (own - r = -(r - own),
-      // negated back through the sign of the scale below).
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double send = f[32 + k];
-        const int lo = __shfl_xor_sync(0xffffffffu, __double2loint(send), 1);
-        const int hi = __shfl_xor_sync(0xffffffffu, __double2hiint(send), 1);
-        const double r = __hiloint2double(hi, lo);
-        const double u = f[k];
-        f[k] = u + r;
-        f[32 + k] = u - r;
-      }
-      // RN32(RN64(S / sqrt n)) as one F2F of RN64(S * RN64(1/sqrt n)); the two
-      // differ only within 4 ulp64 of an f32 rounding midpoint (numerics.cuh).
-      // B's second half is scaled by -hk (RN is sign-symmetric; an exact zero
-      // comes out as -0 there, made +0 in the group min / max below).
-      const double hk2 = half ? -a.hk : a.hk;
-      bool mid = false;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const double q = f[i] * (i < 32 ? a.hk : hk2);
-        mid |= ((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x0FFFFFFCu <= 8u;
-        y[i] = __double2float_rn(q);
-      }
-      need_fix = !row_ok || mid;
-      need_fix |= __shfl_xor_sync(0xffffffffu, (int)need_fix, 1) != 0;
-      if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       cb0 = 32 * half;
       cb1 = 64 + 32 * half;
       hadlayout = true;
@@ -586,6 +798,51 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
       cb1 = 64 * half + 32;
     }
     float mn0, mx0, mn1, mx1;
+    if constexpr (CERT) {
+      minmax32_3(y, mn0, mx0);
+      minmax32_3(y + 32, mn1, mx1);
+      mn1 = __fadd_rn(mn1, 0.0f);  // -0 from the negated half -> +0
+      mx1 = __fadd_rn(mx1, 0.0f);
+      int w;
+      int64_t bit;
+      token_row_pos(g, a.heads, lh, t, w, bit);
+      unsigned short s0, z0, s1, z1;
+      bool ok = cert_group(y, mn0, mx0, Dcert, w, a.rl[w], s0, z0);
+      ok = cert_group(y + 32, mn1, mx1, Dcert, w, a.rl[w], s1, z1) && ok;
+      if (valid) {
+        scales[row * 4 + half] = __ushort_as_half(s0);
+        zeros[row * 4 + half] = __ushort_as_half(z0);
+        scales[row * 4 + 2 + half] = __ushort_as_half(s1);
+        zeros[row * 4 + 2 + half] = __ushort_as_half(z1);
+      }
+      const int pok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);  // every lane shuffles (no short circuit)
+      ok = ok && pok != 0;
+      // uncertified rows to the float64 pass (one atomic per warp), rows
+      // with non-finite / huge inputs to the exact fixup pass
+      const bool to64 = row_ok && !ok && half == 0 && valid;
+      const uint32_t m64 = __ballot_sync(0xffffffffu, to64);
+      if (m64) {
+        const int lane = threadIdx.x & 31, lead = __ffs(m64) - 1;
+        uint32_t base = 0;
+        if (lane == lead) base = atomicAdd(a.fix1_count, (uint32_t)__popc(m64));
+        base = __shfl_sync(0xffffffffu, base, lead);
+        if (to64) a.fix1_rows[base + __popc(m64 & ((1u << lane) - 1u))] = (int32_t)row;
+      }
+      if (!row_ok && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
+      need_fix = !row_ok || !ok;
+      if (valid) {
+        uint8_t* out = a.packed + (bit >> 3);
+        if constexpr (W == 0) {
+          pack32_dispatch(w, y, out + cb0 * w / 8);
+          pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+        } else {
+          pack32_store<W>(y, out + cb0 * W / 8);
+          pack32_store<W>(y + 32, out + cb1 * W / 8);
+        }
+      }
+      if (need_fix) flags = flags_before;
+      continue;
+    }
     if (MODE == M_IDENTITY && !F32) {
       // exact bf16 min/max, two per instruction; NaN / inf surface here
       minmax32_bf16(wv, mn0, mx0);
@@ -626,6 +883,65 @@ __global__ void __launch_bounds__(kThreads, (MODE == M_HADAMARD || MODE == M_DEL
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
+  flags = __reduce_or_sync(__activemask(), flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
+}
+
+// The float64 pass behind the certified encoder: the rows it listed
+// (fix1_rows, count on the device) re-encoded with had64_row -- the
+// reference's butterfly in stage order and the exact rounding of the
+// uncertified kernel -- read straight from global memory (a thread pair per
+// row); rows this pass cannot prove exact go on to k_encode_fixup.
+template <int G, int W>
+__global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
+  const uint32_t n = *a.fix1_count;
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, half = tid & 1;
+  __half* scales = reinterpret_cast<__half*>(a.meta);
+  __half* zeros = scales + g.ngroups;
+  uint32_t flags = 0;
+  float nanacc = 0.0f;
+  for (int64_t base = (int64_t)blockIdx.x * kRows; base < (int64_t)n; base += (int64_t)gridDim.x * kRows) {
+    const int64_t e = base + (tid >> 1);
+    const bool valid = e < (int64_t)n;  // the others repeat row `base` and store nothing
+    const int64_t row = a.fix1_rows[valid ? e : base];
+    const int64_t lh = row / g.T, t = row - lh * g.T;
+    const int64_t off = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + off);
+    uint32_t wv[32];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint4 c = __ldg(src + k);
+      wv[4 * k] = c.x; wv[4 * k + 1] = c.y; wv[4 * k + 2] = c.z; wv[4 * k + 3] = c.w;
+    }
+    const uint32_t flags_before = flags;
+    __align__(8) float y[64];
+    const bool need_fix = had64_row<false>(wv, half, a, y, nanacc);
+    if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
+    float mn0, mx0, mn1, mx1;
+    minmax32(y, mn0, mx0);
+    minmax32(y + 32, mn1, mx1);
+    mn1 = __fadd_rn(mn1, 0.0f);
+    mx1 = __fadd_rn(mx1, 0.0f);
+    int w;
+    int64_t bit;
+    token_row_pos(g, a.heads, lh, t, w, bit);
+    const int cb0 = 32 * half, cb1 = 64 + 32 * half;
+    quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
+                  true, half, flags);
+    if (valid) {
+      uint8_t* out = a.packed + (bit >> 3);
+      if constexpr (W == 0) {
+        pack32_dispatch(w, y, out + cb0 * w / 8);
+        pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+      } else {
+        pack32_store<W>(y, out + cb0 * W / 8);
+        pack32_store<W>(y + 32, out + cb1 * W / 8);
+      }
+    }
+    if (need_fix) flags = flags_before;
+  }
+  if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
@@ -1053,15 +1369,29 @@ template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   constexpr int smem = enc_smem_bytes<F32>();
   auto k = k_enc128<MODE, G, W, F32, false>;
-  if constexpr (!F32) {
-    if (a.paged) {
-      k = k_enc128<MODE, G, W, false, true>;
-      set_max_dyn_smem<k_enc128<MODE, G, W, false, true>>(smem);
-    } else {
-      set_max_dyn_smem<k_enc128<MODE, G, W, false, false>>(smem);
+  const bool cert = MODE == M_HADAMARD && !F32 && G == 32 && a.fix1_rows != nullptr;
+  if constexpr (MODE == M_HADAMARD && !F32 && G == 32) {
+    if (cert) {
+      if (a.paged) {
+        k = k_enc128<MODE, G, W, false, true, true>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, true, true>>(smem);
+      } else {
+        k = k_enc128<MODE, G, W, false, false, true>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, false, true>>(smem);
+      }
     }
-  } else {
-    set_max_dyn_smem<k_enc128<MODE, G, W, F32, false>>(smem);
+  }
+  if (!cert) {
+    if constexpr (!F32) {
+      if (a.paged) {
+        k = k_enc128<MODE, G, W, false, true>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, true>>(smem);
+      } else {
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, false>>(smem);
+      }
+    } else {
+      set_max_dyn_smem<k_enc128<MODE, G, W, F32, false>>(smem);
+    }
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
@@ -1217,6 +1547,26 @@ bool fast128_applicable(const Geo& g) {
   return true;
 }
 
+template <int W>
+cudaError_t launch_had64_list_w(const EncArgs& a, int sm_count, cudaStream_t s) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had64_list<32, W>, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  k_had64_list<32, W><<<(unsigned)(sm_count * per_sm), kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// the float64 pass over the rows the certified encoder listed
+cudaError_t launch_had64_list(const EncArgs& a, int sm_count, cudaStream_t s) {
+  ProfScope ps("encode_had64_list", s);
+  switch (a.g.quant == Q_UNIFORM ? a.g.bits : 0) {
+    case 2: return launch_had64_list_w<2>(a, sm_count, s);
+    case 4: return launch_had64_list_w<4>(a, sm_count, s);
+    case 8: return launch_had64_list_w<8>(a, sm_count, s);
+    default: return launch_had64_list_w<0>(a, sm_count, s);
+  }
+}
+
 cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s) {
   const bool f32 = a.g.in_dtype == KVC_DTYPE_F32;
   const int64_t nrows = a.g.LH * a.g.T;
@@ -1229,8 +1579,14 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
   } else if (!(f32 ? make_input_map_f32(&map, a.kv, nrows) : make_input_map(&map, a.kv, nrows))) {
     return launch_encode_generic(a, s);
   }
-  ProfScope ps("encode_fast128", s);
-  return f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
+  cudaError_t e;
+  {
+    ProfScope ps("encode_fast128", s);
+    e = f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
+  }
+  if (e == cudaSuccess && !f32 && a.fix1_rows && a.g.transform == T_HADAMARD && a.g.group == 32)
+    e = launch_had64_list(a, sm_count, s);
+  return e;
 }
 
 cudaError_t launch_decode_fast128(const DecArgs& a, int sm_count, cudaStream_t s) {

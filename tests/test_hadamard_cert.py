@@ -1,0 +1,142 @@
+"""The certified float32 Hadamard encoder (fast128.cu: had32_row / cert_group).
+
+The hot path of the reference default profile (transforms.py:62 then
+quantize.py:142-154 at 32-channel groups) runs the butterfly in float32 and
+accepts a row only when every quantizer decision is provably the one the
+reference's float64 butterfly leads to; other rows go to the float64 pass.
+
+CPU part: a numpy restatement of the certificate (same float32 butterfly,
+same bound D, same interval tests) over 131,072 reference-generator rows --
+every certified row must quantize exactly like the reference, and rows where
+plain float32 would give different bytes must all be rejected.
+GPU part: those rows (plus the certificate's near-miss rows) through the C
+ABI, bit-exact against the oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+
+U = 2.0 ** -24
+C = np.sqrt(128.0)
+R32 = np.float32(1.0 / C)
+
+
+def _bf16(a):
+    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    b = ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return b.view(np.float32)
+
+
+def _fwht32(x):
+    """float32 butterfly in the kernel's stage order (h = 1, 2, .., 64)."""
+    y = np.array(x, dtype=np.float32)
+    n = y.shape[-1]
+    lead = y.shape[:-1]
+    h = 1
+    while h < n:
+        v = y.reshape(*lead, n // (2 * h), 2, h)
+        a, b = v[..., 0, :], v[..., 1, :]
+        y = np.concatenate([(a + b)[..., None, :], (a - b)[..., None, :]], axis=-2).reshape(*lead, n)
+        h <<= 1
+    return y
+
+
+def _f16bits(v):
+    return np.asarray(v, dtype=np.float32).astype(np.float16).view(np.uint16)
+
+
+def certify(x):
+    """(y_hat, certified) per row of bf16-exact x (N, 128), as cert_group."""
+    N = x.shape[0]
+    yh = (_fwht32(x) * R32).astype(np.float32)
+    ax = np.abs(x).astype(np.float64)
+    e = np.frexp(np.where(ax > 0, ax, 0.0))[1] - 1
+    e = np.where(ax > 0, e, -127)
+    kex = np.clip(16 - (e.max(1) - e.min(1)), 0, 7)
+    D = ((10.01 - kex) * U * ax.sum(1) / C * 1.002 + 2.0 ** -140)[:, None]
+    g = yh.reshape(N, 4, 32).astype(np.float64)
+    mn, mx = g.min(-1), g.max(-1)
+    dn = lambda v: np.nextafter(v.astype(np.float32), np.float32(-np.inf))  # noqa: E731
+    up = lambda v: np.nextafter(v.astype(np.float32), np.float32(np.inf))  # noqa: E731
+    zl, zh = _f16bits(dn(mn - D)), _f16bits(up(mn + D))
+    dl, dh = dn(mx - mn - 2 * D).astype(np.float64), up(mx - mn + 2 * D).astype(np.float64)
+    sl, sh = _f16bits(dl / 15 * (1 - 2.0 ** -20)), _f16bits(dh / 15 * (1 + 2.0 ** -20))
+    ok = (zl == zh) & (sl == sh) & (dl > 0)
+    s = sl.view(np.float16).astype(np.float32)
+    z = zl.view(np.float16).astype(np.float32)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = (g.astype(np.float32) - z[..., None]) / np.where(s > 0, s, 1)[..., None]
+        tmax = np.maximum(np.abs((mn - z) / np.where(s > 0, s, 1)), np.abs((mx - z) / np.where(s > 0, s, 1)))
+        tau = D / np.where(s > 0, s, np.inf) * 1.0001 + 2.0 ** -20 * (tmax + 1)
+    rho = np.abs(t - np.rint(t)).max(-1)
+    ok &= (rho < 0.5 - tau) | (s == 0)
+    return yh, ok.all(1)
+
+
+def _rows(n_layers=4):
+    vals, _ = oracle.generate_kv(n_layers, 8, 4096, 128, seed=1)
+    return _bf16(vals).reshape(-1, 128)
+
+
+def _quant(y):
+    sym, sc, zr = oracle.quantize_rows(y.reshape(1, 1, -1, 128), np.array([[4]]), 32)
+    n = y.shape[0]
+    return sym.reshape(n, -1), sc.reshape(n, -1).view(np.uint16), zr.reshape(n, -1).view(np.uint16)
+
+
+def test_certificate_is_sound_on_reference_rows():
+    x = _rows()
+    yref = (oracle.fwht64(x) / C).astype(np.float32)
+    yh, cert = certify(x)
+    a, b = _quant(yref), _quant(yh)
+    same = np.ones(x.shape[0], bool)
+    for p, q in zip(a, b):
+        same &= (p == q).all(1)
+    # float32 alone is wrong on some rows; the certificate rejects every one
+    assert (~same).sum() > 0
+    assert not (cert & ~same).any()
+    # and keeps the float64 pass small (3 % of rows on this distribution)
+    assert cert.mean() > 0.95
+
+
+def _hard_rows():
+    """Rows where plain float32 bytes differ from the reference, plus the
+    rejected rows closest to certification (64 rows in all)."""
+    x = _rows()
+    yref = (oracle.fwht64(x) / C).astype(np.float32)
+    yh, cert = certify(x)
+    a, b = _quant(yref), _quant(yh)
+    same = np.ones(x.shape[0], bool)
+    for p, q in zip(a, b):
+        same &= (p == q).all(1)
+    wrong = np.flatnonzero(~same)
+    rejected = np.flatnonzero(~cert & same)
+    take = np.concatenate([wrong, rejected[: 64 - len(wrong)], np.flatnonzero(cert)[:64]])[:128]
+    return x[take], len(wrong)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sid", ["t=hadamard;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=2,g=32;c=entropy",
+                                 "t=hadamard;q=mixed,hi=8,lo=2,g=32,rho=0.5;c=none"])
+def test_gpu_certified_encoder_on_hard_rows(sid):
+    import torch
+
+    from paper_2605_13734_b200 import KVCodec
+
+    rows, nwrong = _hard_rows()
+    assert nwrong > 0
+    shape = (2, 1, rows.shape[0] // 2, 128)
+    vb = rows.reshape(shape)
+    imp = np.array([[0.9], [0.1]])
+    s = oracle.parse_id(sid)
+    cls = oracle.classify_heads(imp, s.rho) if s.quant == "mixed" else None
+    ref = oracle.encode_blob(vb, imp, sid, block=256)
+    codec = KVCodec(sid, shape, block_symbols=256)
+    blob = codec.encode(torch.from_numpy(vb).to(torch.bfloat16).cuda(), head_classes=cls)
+    codec.check()
+    assert blob.metadata_bytes() == ref["metadata"]
+    assert blob.payload_bytes() == ref["payload"]
