@@ -490,34 +490,27 @@ __device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushor
 // Float32 Hadamard of the row held by a thread pair (this thread: channels
 // 64*half..+63 as bf16 pairs in wv).  y gets this thread's 64 outputs
 // (chunk 0: channels 32*half.., chunk 1: 64 + 32*half.., the same layout as
-// had64_row; B's chunk 1 as -(-y), an exact zero there as -0); returns D.
-// row_ok: no non-finite input and every |x| < 2^101 (no float32 overflow).
+// had64_row; B's chunk 1 as -(-y), an exact zero there as -0).  Returns the
+// row's bound D, or -1 when every stage was exact (the caller then bounds
+// each group by 3.01 u max|y| of that group: only the scaling and the
+// reference's roundings remain).  row_ok: finite inputs with Sum|x| < 2^100
+// (no float32 overflow anywhere in the butterfly).
 __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc,
                                            bool& row_ok) {
-  int kex;
-  {
-    uint32_t amx = wv[0] & 0x7FFF7FFFu, amn = amx;
-#pragma unroll
-    for (int k = 1; k < 32; ++k) {
-      const uint32_t aw = wv[k] & 0x7FFF7FFFu;
-      amx = bmax2(amx, aw);
-      amn = bmin2(amn, aw);
-    }
-    amx = bmax2(amx, __byte_perm(amx, 0, 0x1032));
-    amn = bmin2(amn, __byte_perm(amn, 0, 0x1032));
-    if ((amx & 0x7F80u) == 0x7F80u) nanacc = 1.0f;
-    amx = bmax2(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
-    amn = bmin2(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
-    const int emax = (int)((amx >> 7) & 0xFFu), emin = (int)((amn >> 7) & 0xFFu);
-    row_ok = emax <= 127 + 100;
-    kex = min(max(16 - (emax - emin), 0), 7);
-  }
   // P[m] = (local m, local m + 32): stages h = 1..16 pair P[m] with P[m + h]
   float2 P[32];
 #pragma unroll
   for (int m = 0; m < 32; ++m)
     P[m] = make_float2(__uint_as_float(vbits_of<false>(wv, m)), __uint_as_float(vbits_of<false>(wv, m + 32)));
-  // h = 1, and Sum|x| as max(|a + b|, |a - b|) = |a| + |b| per pair
+  // max / min |x| (three per FMNMX3, |.| free), for the exponent span
+  float amx = fmaxf(fabsf(P[0].x), fabsf(P[0].y)), amn = fminf(fabsf(P[0].x), fabsf(P[0].y));
+#pragma unroll
+  for (int m = 1; m < 32; ++m) {
+    amx = max3f(amx, fabsf(P[m].x), fabsf(P[m].y));
+    amn = min3f(amn, fabsf(P[m].x), fabsf(P[m].y));
+  }
+  // h = 1, and Sum|x| as max(|a + b|, |a - b|) = |a| + |b| per pair (a NaN
+  // input makes the sum NaN)
   float2 sa = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int m = 0; m < 32; m += 2) {
@@ -562,6 +555,19 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
   }
   float s1 = sa.x + sa.y;
   s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+  amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
+  amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
+  if (!(amx <= 3.40282347e38f) || s1 != s1) nanacc = 1.0f;  // inf / NaN input (tensors.py:41-42)
+  row_ok = s1 < 0x1p100f;
+  // Exact stages: inputs are multiples of 2^(emin-7); after k stages every
+  // partial sum is below min(2^(emax+1+k), 2^(es1+1)) (es1: exponent of an
+  // upper bound of Sum|x|), and fits 24 bits when that exponent is at most
+  // emin + 17.  The bound is nondecreasing in k, so the exact stages are a
+  // prefix: all seven when es1 <= emin + 16, else 16 - (emax - emin) of them.
+  const int emax = (int)(__float_as_uint(amx) >> 23), emin = (int)(__float_as_uint(amn) >> 23);
+  const int es1 = (int)(__float_as_uint(s1 * 1.0000153f) >> 23);  // s1 (1 + 2^-16) >= Sum|x|
+  if (es1 <= emin + 16) return -1.0f;
+  const int kex = min(max(16 - (emax - emin), 0), 7);
   // (10.01 - kex) u / c, rounded up generously (1.002 covers the float32
   // evaluation of Sum|x| and of this coefficient)
   const float coef = (10.01f - (float)kex) * 0x1p-24f * a.hr32 * 1.002f;
@@ -575,6 +581,8 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
 __device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float D, int w, float rl,
                                            unsigned short& s16, unsigned short& z16) {
   const float lv = (float)((1 << w) - 1);
+  // exact butterfly: |y_hat - y| <= 3.01 u |S_j| / c <= 3.01 u max|y_hat| (1 + 2.1u) of the group
+  if (D < 0.0f) D = __fmaf_ru(fmaxf(fabsf(mn), fabsf(mx)), 3.02f * 0x1p-24f, 0x1p-140f);
   // zero RN16(min y), min y in [mn - D, mn + D]
   const unsigned short zl = rn16(__fsub_rd(mn, D)), zh = rn16(__fadd_ru(mn, D));
   // scale RN16(RN64(RN32(max - min) / lv)), RN32(max - min) in [dl, dh]
@@ -595,16 +603,18 @@ __device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float 
   const bool easy = l1 >= -0.5f && h1 < lv + 0.5f;
   float racc = 0.0f;
   float2* y2 = reinterpret_cast<float2*>(yy);
-  const float2 nz = f2(-z, -z), rr = f2(r, r), ns = f2(-s, -s), mg = f2(kMagicRound, kMagicRound);
+  const float2 nz = f2(-z, -z), rr = f2(r, r), mg = f2(kMagicRound, kMagicRound);
   const float2 nmg = f2(-kMagicRound, -kMagicRound);
+  // symbols rint(RN(RN(y - z) r)): within 5.1u |t| of the reference's
+  // rint(RN(RN(y - z) / s)) argument, inside tau's 2^-20 (|t| + 1), so a
+  // quotient farther than tau from its rounding boundary needs no Markstein
+  // correction (quant_magic) to round like the reference
   if (__all_sync(0xffffffffu, easy)) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 d = f2add(y2[i], nz);
-      const float2 q0 = f2mul(d, rr);
-      const float2 q1 = f2fma(f2fma(q0, ns, d), rr, q0);
-      const float2 m = f2add(q1, mg);
-      const float2 rho = f2sub(q1, f2add(m, nmg));
+      const float2 q = f2mul(f2add(y2[i], nz), rr);
+      const float2 m = f2add(q, mg);
+      const float2 rho = f2sub(q, f2add(m, nmg));
       racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
       y2[i] = m;
     }
@@ -612,11 +622,9 @@ __device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float 
     const float top = kMagicRound + lv;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 d = f2add(y2[i], nz);
-      const float2 q0 = f2mul(d, rr);
-      const float2 q1 = f2fma(f2fma(q0, ns, d), rr, q0);
-      const float2 m = f2add(q1, mg);
-      const float2 rho = f2sub(q1, f2add(m, nmg));
+      const float2 q = f2mul(f2add(y2[i], nz), rr);
+      const float2 m = f2add(q, mg);
+      const float2 rho = f2sub(q, f2add(m, nmg));
       racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
       y2[i] = f2(fminf(fmaxf(m.x, kMagicRound), top), fminf(fmaxf(m.y, kMagicRound), top));
     }
@@ -646,12 +654,16 @@ __host__ __device__ constexpr int enc_smem_bytes() {
 // separate instantiation so the contiguous kernels keep their exact code
 // CERT: the certified float32 Hadamard (bf16, G = 32) with the float64 pass
 // behind it for the rows it cannot certify
-template <int MODE, int G, int W, bool F32 = false, bool PAGED = false, bool CERT = false>
+// (4 CTAs per SM; 5, with a 2-stage ring and 96 registers, measured the same)
+template <int MODE, int G, int W, bool F32 = false, bool PAGED = false, int CERT = 0>
 __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   static_assert(!(F32 && PAGED), "paged input is bf16");
-  static_assert(!CERT || (MODE == M_HADAMARD && !F32 && G == 32), "certified path: bf16 Hadamard, 32-channel groups");
+  static_assert(CERT == 0 || (MODE == M_HADAMARD && !F32 && G == 32), "certified path: bf16 Hadamard, 32-channel groups");
   constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
+  // certified path: a slot is refilled by the last warp to copy it out (a
+  // per-slot arrival counter) instead of after a CTA barrier
+  __shared__ uint32_t slot_arrivals[NS];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(tiles + NS * TB);
@@ -664,7 +676,10 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
   // fp32 quarter rows)
   constexpr int kBoxRows = F32 ? 4 * kRows : 2 * kRows;
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      slot_arrivals[s] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -689,6 +704,8 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
   uint32_t flags = 0;
   float nanacc = 0.0f;
   int it = 0;
+  uint32_t pend_mask = 0, pend_base = 0;  // certified path: last tile's list append
+  int32_t pend_row = 0;
   // this thread's values from a tile row (swizzled 128-byte box rows); w[]
   // holds 32 bf16 pairs or 64 fp32 bit patterns
   auto load_half = [&](const uint8_t* tb, int r, uint32_t* w) {
@@ -735,12 +752,29 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
         }
       }
     }
-    __syncthreads();  // every thread has its half-row in registers: slot s is free
-    if (tid == 0) {
-      const int64_t next = tile + (int64_t)NS * gridDim.x;
-      if (next < ntiles) {
-        fence_proxy_async();
-        issue(s, next);
+    if constexpr (CERT != 0) {
+      // this warp's half rows are in registers; the warp completing the
+      // slot's four arrivals (a monotonic count) refills it
+      __syncwarp();
+      if ((tid & 31) == 0) {
+        __threadfence_block();
+        if ((atomicAdd(&slot_arrivals[s], 1u) & (kThreads / 32 - 1)) == kThreads / 32 - 1) {
+          __threadfence_block();
+          const int64_t next = tile + (int64_t)NS * gridDim.x;
+          if (next < ntiles) {
+            fence_proxy_async();
+            issue(s, next);
+          }
+        }
+      }
+    } else {
+      __syncthreads();  // every thread has its half-row in registers: slot s is free
+      if (tid == 0) {
+        const int64_t next = tile + (int64_t)NS * gridDim.x;
+        if (next < ntiles) {
+          fence_proxy_async();
+          issue(s, next);
+        }
       }
     }
     // invalid tail rows run the same code (shuffles need the full warp) but
@@ -819,15 +853,16 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       ok = ok && pok != 0;
       // uncertified rows to the float64 pass (one atomic per warp), rows
       // with non-finite / huge inputs to the exact fixup pass
-      const bool to64 = row_ok && !ok && half == 0 && valid;
-      const uint32_t m64 = __ballot_sync(0xffffffffu, to64);
-      if (m64) {
-        const int lane = threadIdx.x & 31, lead = __ffs(m64) - 1;
-        uint32_t base = 0;
-        if (lane == lead) base = atomicAdd(a.fix1_count, (uint32_t)__popc(m64));
-        base = __shfl_sync(0xffffffffu, base, lead);
-        if (to64) a.fix1_rows[base + __popc(m64 & ((1u << lane) - 1u))] = (int32_t)row;
+      // (the atomic's result is consumed one tile later, off the critical path)
+      const int lane = threadIdx.x & 31;
+      if (pend_mask) {
+        const uint32_t base = __shfl_sync(0xffffffffu, pend_base, __ffs(pend_mask) - 1);
+        if ((pend_mask >> lane) & 1u) a.fix1_rows[base + __popc(pend_mask & ((1u << lane) - 1u))] = pend_row;
       }
+      const bool to64 = row_ok && !ok && half == 0 && valid;
+      pend_mask = __ballot_sync(0xffffffffu, to64);
+      pend_row = (int32_t)row;
+      if (pend_mask && lane == __ffs(pend_mask) - 1) pend_base = atomicAdd(a.fix1_count, (uint32_t)__popc(pend_mask));
       if (!row_ok && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       need_fix = !row_ok || !ok;
       if (valid) {
@@ -880,6 +915,13 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       }
     }
     if (need_fix) flags = flags_before;  // the fixup pass sets this row's flags exactly
+  }
+  if constexpr (CERT != 0) {
+    if (pend_mask) {
+      const int lane = threadIdx.x & 31;
+      const uint32_t base = __shfl_sync(0xffffffffu, pend_base, __ffs(pend_mask) - 1);
+      if ((pend_mask >> lane) & 1u) a.fix1_rows[base + __popc(pend_mask & ((1u << lane) - 1u))] = pend_row;
+    }
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
@@ -1373,11 +1415,11 @@ cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, c
   if constexpr (MODE == M_HADAMARD && !F32 && G == 32) {
     if (cert) {
       if (a.paged) {
-        k = k_enc128<MODE, G, W, false, true, true>;
-        set_max_dyn_smem<k_enc128<MODE, G, W, false, true, true>>(smem);
+        k = k_enc128<MODE, G, W, false, true, 1>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, true, 1>>(smem);
       } else {
-        k = k_enc128<MODE, G, W, false, false, true>;
-        set_max_dyn_smem<k_enc128<MODE, G, W, false, false, true>>(smem);
+        k = k_enc128<MODE, G, W, false, false, 1>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, false, false, 1>>(smem);
       }
     }
   }
