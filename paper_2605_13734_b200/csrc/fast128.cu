@@ -488,9 +488,9 @@ __device__ __forceinline__ void minmax32_3(const float* y, float& mn, float& mx)
 __device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushort(__float2half_rn(v)); }
 
 // Float32 Hadamard of the row held by a thread pair (this thread: channels
-// 64*half..+63 as bf16 pairs in wv).  y gets this thread's 64 outputs
-// (chunk 0: channels 32*half.., chunk 1: 64 + 32*half.., the same layout as
-// had64_row; B's chunk 1 as -(-y), an exact zero there as -0).  Returns the
+// 64*half..+63 as bf16 pairs in wv).  y gets this thread's 64 unscaled sums
+// S (chunk 0: channels 32*half.., chunk 1: 64 + 32*half.., the same layout
+// as had64_row; B's chunk 1 negated).  Returns the
 // row's bound D, or -1 when every stage was exact (the caller then bounds
 // each group by 3.01 u max|y| of that group: only the scaling and the
 // reference's roundings remain).  row_ok: finite inputs with Sum|x| < 2^100
@@ -502,13 +502,10 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
 #pragma unroll
   for (int m = 0; m < 32; ++m)
     P[m] = make_float2(__uint_as_float(vbits_of<false>(wv, m)), __uint_as_float(vbits_of<false>(wv, m + 32)));
-  // max / min |x| (three per FMNMX3, |.| free), for the exponent span
-  float amx = fmaxf(fabsf(P[0].x), fabsf(P[0].y)), amn = fminf(fabsf(P[0].x), fabsf(P[0].y));
+  // min |x| (three per FMNMX3, |.| free): the inputs' 2^(emin-7) grid
+  float amn = fminf(fabsf(P[0].x), fabsf(P[0].y));
 #pragma unroll
-  for (int m = 1; m < 32; ++m) {
-    amx = max3f(amx, fabsf(P[m].x), fabsf(P[m].y));
-    amn = min3f(amn, fabsf(P[m].x), fabsf(P[m].y));
-  }
+  for (int m = 1; m < 32; ++m) amn = min3f(amn, fabsf(P[m].x), fabsf(P[m].y));
   // h = 1, and Sum|x| as max(|a + b|, |a - b|) = |a| + |b| per pair (a NaN
   // input makes the sum NaN)
   float2 sa = make_float2(0.0f, 0.0f);
@@ -539,15 +536,13 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
     K[m] = __fmaf_rn(P[m].y, sg, P[m].x);
     Y[m] = __fmaf_rn(P[m].y, -sg, P[m].x);
   }
-  // h = 64 across the pair, then the scaling by RN32(1/c) (-RN32(1/c) for
-  // B's negated chunk 1)
-  const float2 r2 = make_float2(a.hr32, a.hr32);
-  const float2 n2 = half ? make_float2(-a.hr32, -a.hr32) : r2;
+  // h = 64 across the pair: the unscaled sums S (B's chunk 1 as -S); the
+  // scaling by RN32(1/c) happens inside the quantizer (cert_group)
 #pragma unroll
   for (int m = 0; m < 32; m += 2) {
     const float2 rv = make_float2(__shfl_xor_sync(0xffffffffu, Y[m], 1), __shfl_xor_sync(0xffffffffu, Y[m + 1], 1));
     const float2 kv = make_float2(K[m], K[m + 1]);
-    const float2 s = f2mul(f2add(kv, rv), r2), d = f2mul(f2sub(kv, rv), n2);
+    const float2 s = f2add(kv, rv), d = f2sub(kv, rv);
     y[m] = s.x;
     y[m + 1] = s.y;
     y[32 + m] = d.x;
@@ -555,30 +550,28 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
   }
   float s1 = sa.x + sa.y;
   s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-  amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, 1));
   amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
-  if (!(amx <= 3.40282347e38f) || s1 != s1) nanacc = 1.0f;  // inf / NaN input (tensors.py:41-42)
+  // a NaN / inf input (or a sum near the float32 range) makes s1 NaN / huge:
+  // the row goes to the exact fixup pass, which also raises the input flag
   row_ok = s1 < 0x1p100f;
-  // Exact stages: inputs are multiples of 2^(emin-7); after k stages every
-  // partial sum is below min(2^(emax+1+k), 2^(es1+1)) (es1: exponent of an
-  // upper bound of Sum|x|), and fits 24 bits when that exponent is at most
-  // emin + 17.  The bound is nondecreasing in k, so the exact stages are a
-  // prefix: all seven when es1 <= emin + 16, else 16 - (emax - emin) of them.
-  const int emax = (int)(__float_as_uint(amx) >> 23), emin = (int)(__float_as_uint(amn) >> 23);
+  // Exact stages: inputs are multiples of 2^(emin-7); every partial sum is
+  // below 2^(es1+1) (es1: exponent of an upper bound of Sum|x|), so all
+  // seven stages are exact when es1 <= emin + 16 (24 bits); other rows take
+  // the gamma_7 bound
+  const int emin = (int)(__float_as_uint(amn) >> 23);
   const int es1 = (int)(__float_as_uint(s1 * 1.0000153f) >> 23);  // s1 (1 + 2^-16) >= Sum|x|
   if (es1 <= emin + 16) return -1.0f;
-  const int kex = min(max(16 - (emax - emin), 0), 7);
-  // (10.01 - kex) u / c, rounded up generously (1.002 covers the float32
-  // evaluation of Sum|x| and of this coefficient)
-  const float coef = (10.01f - (float)kex) * 0x1p-24f * a.hr32 * 1.002f;
-  return __fmaf_ru(s1, coef, 0x1p-140f);
+  // 10.01 u / c, rounded up generously (1.002 covers the float32 evaluation
+  // of Sum|x| and of this coefficient)
+  return __fmaf_ru(s1, 10.01f * 0x1p-24f * a.hr32 * 1.002f, 0x1p-140f);
 }
 
-// Quantize one certified group of 32 values (yy -> magic floats 2^23 + 1.5
-// 2^23 + symbol, as quantize64) with fp16 scale / zero s16 / z16; returns
+// Quantize one certified group of 32 unscaled sums (y = S sc, sc = +-RN32(1/c);
+// yy -> magic floats 1.5 2^23 + symbol, as quantize64) with fp16 scale /
+// zero s16 / z16; mn / mx: min / max of y.  Returns
 // false when a decision is not constant over +-D (the row is then re-encoded
 // by the float64 pass, which also rewrites s16 / z16).
-__device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float D, int w, float rl,
+__device__ __forceinline__ bool cert_group(float* yy, float sc, float mn, float mx, float D, int w, float rl,
                                            unsigned short& s16, unsigned short& z16) {
   const float lv = (float)((1 << w) - 1);
   // exact butterfly: |y_hat - y| <= 3.01 u |S_j| / c <= 3.01 u max|y_hat| (1 + 2.1u) of the group
@@ -603,16 +596,16 @@ __device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float 
   const bool easy = l1 >= -0.5f && h1 < lv + 0.5f;
   float racc = 0.0f;
   float2* y2 = reinterpret_cast<float2*>(yy);
-  const float2 nz = f2(-z, -z), rr = f2(r, r), mg = f2(kMagicRound, kMagicRound);
+  const float2 nz = f2(-z, -z), rr = f2(r, r), sc2 = f2(sc, sc), mg = f2(kMagicRound, kMagicRound);
   const float2 nmg = f2(-kMagicRound, -kMagicRound);
-  // symbols rint(RN(RN(y - z) r)): within 5.1u |t| of the reference's
-  // rint(RN(RN(y - z) / s)) argument, inside tau's 2^-20 (|t| + 1), so a
-  // quotient farther than tau from its rounding boundary needs no Markstein
-  // correction (quant_magic) to round like the reference
+  // symbols rint(RN(RN(S sc - z) r)): within D / s + 5.1u |t| of the
+  // reference's rint(RN(RN(y - z) / s)) argument (D covers the scaling),
+  // inside tau, so a quotient farther than tau from its rounding boundary
+  // needs no Markstein correction (quant_magic) to round like the reference
   if (__all_sync(0xffffffffu, easy)) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 q = f2mul(f2add(y2[i], nz), rr);
+      const float2 q = f2mul(f2fma(y2[i], sc2, nz), rr);
       const float2 m = f2add(q, mg);
       const float2 rho = f2sub(q, f2add(m, nmg));
       racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
@@ -622,7 +615,7 @@ __device__ __forceinline__ bool cert_group(float* yy, float mn, float mx, float 
     const float top = kMagicRound + lv;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const float2 q = f2mul(f2add(y2[i], nz), rr);
+      const float2 q = f2mul(f2fma(y2[i], sc2, nz), rr);
       const float2 m = f2add(q, mg);
       const float2 rho = f2sub(q, f2add(m, nmg));
       racc = max3f(racc, fabsf(rho.x), fabsf(rho.y));
@@ -833,16 +826,22 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     }
     float mn0, mx0, mn1, mx1;
     if constexpr (CERT) {
-      minmax32_3(y, mn0, mx0);
-      minmax32_3(y + 32, mn1, mx1);
-      mn1 = __fadd_rn(mn1, 0.0f);  // -0 from the negated half -> +0
-      mx1 = __fadd_rn(mx1, 0.0f);
+      // min / max of y = RN(S sc): RN is monotone, so scale the extremes of S
+      // (B's chunk 1 holds -S: its scale -RN32(1/c) swaps them)
+      float sn0, sx0, sn1, sx1;
+      minmax32_3(y, sn0, sx0);
+      minmax32_3(y + 32, sn1, sx1);
+      const float sc0 = a.hr32, sc1 = half ? -a.hr32 : a.hr32;
+      mn0 = __fmul_rn(sn0, sc0);
+      mx0 = __fmul_rn(sx0, sc0);
+      mn1 = __fadd_rn(__fmul_rn(half ? sx1 : sn1, sc1), 0.0f);  // -0 from the negation -> +0
+      mx1 = __fadd_rn(__fmul_rn(half ? sn1 : sx1, sc1), 0.0f);
       int w;
       int64_t bit;
       token_row_pos(g, a.heads, lh, t, w, bit);
       unsigned short s0, z0, s1, z1;
-      bool ok = cert_group(y, mn0, mx0, Dcert, w, a.rl[w], s0, z0);
-      ok = cert_group(y + 32, mn1, mx1, Dcert, w, a.rl[w], s1, z1) && ok;
+      bool ok = cert_group(y, sc0, mn0, mx0, Dcert, w, a.rl[w], s0, z0);
+      ok = cert_group(y + 32, sc1, mn1, mx1, Dcert, w, a.rl[w], s1, z1) && ok;
       if (valid) {
         scales[row * 4 + half] = __ushort_as_half(s0);
         zeros[row * 4 + half] = __ushort_as_half(z0);
@@ -950,6 +949,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
     const int64_t lh = row / g.T, t = row - lh * g.T;
     const int64_t off = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + off);
+    {  // the next iteration's half row into L2 while this one computes
+      const int64_t en = e + (int64_t)gridDim.x * kRows;
+      if (en < (int64_t)n) {
+        const int64_t rn = a.fix1_rows[en], lhn = rn / g.T;
+        const int64_t offn = a.paged ? out_index(a, lhn, rn - lhn * g.T, half * 64) : rn * 128 + half * 64;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint16_t*>(a.kv) + offn));
+      }
+    }
     uint32_t wv[32];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
