@@ -403,13 +403,14 @@ int kvc_plan_create(kvc_plan** out, const char* strategy_id, int64_t L, int64_t 
     p.ws_delta = off;
     off = align_up(off + delta128_ws_bytes(g), 256);
   }
-  // fused Hadamard encode: two row lists (one int32 per token row at most
-  // each, counts in a shared 16-byte header): rows the certified float32
-  // pass hands to the float64 pass, and rows left to the exact fixup pass
+  // fused Hadamard encode: the list of rows left to the exact fixup pass
+  // (count + one int32 per token row at most), then a bitmap of the rows the
+  // certified float32 pass hands to the float64 pass (one bit per token row)
   p.ws_fix = -1;
   if (g.transform == T_HADAMARD && fast128_applicable(g)) {
     p.ws_fix = off;
-    off = align_up(off + 16 + 8 * g.LH * g.T, 256);
+    off = align_up(off + 16 + 4 * g.LH * g.T, 16);
+    off = align_up(off + 4 * ((g.LH * g.T + 31) / 32), 256);
   }
   p.ws_bytes = off;
   snprintf(p.id, sizeof p.id, "%s", canon.c_str());
@@ -600,11 +601,12 @@ static int encode_impl(const kvc_plan* plan, const void* kv, int paged, const in
     a.fix_rows = reinterpret_cast<int32_t*>(ws + p.ws_fix + 16);
     // KVC_HADAMARD_FP64=1 keeps every row on the float64 encoder (A/B runs)
     static const bool fp64_only = getenv("KVC_HADAMARD_FP64") && atoi(getenv("KVC_HADAMARD_FP64")) != 0;
+    if ((e = cudaMemsetAsync(a.fix_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e, "memset");
     if (!fp64_only) {
-      a.fix1_count = a.fix_count + 1;
-      a.fix1_rows = a.fix_rows + g.LH * g.T;
+      a.fix1_bits = reinterpret_cast<uint32_t*>(ws + align_up(p.ws_fix + 16 + 4 * g.LH * g.T, 16));
+      if ((e = cudaMemsetAsync(a.fix1_bits, 0, 4 * ((g.LH * g.T + 31) / 32), s)) != cudaSuccess)
+        return cuda_fail(e, "memset");
     }
-    if ((e = cudaMemsetAsync(a.fix_count, 0, 8, s)) != cudaSuccess) return cuda_fail(e, "memset");
   }
   if (fast128_applicable(g))
     e = launch_encode_fast128(a, p.sm_count, s);

@@ -459,7 +459,7 @@ __device__ __forceinline__ bool had64_row(const uint32_t* wv, int half, const En
 // subnormal intermediates below 2^-146 in all.  A group is certified when
 // every decision is constant on [y_hat - D, y_hat + D]: the zero and the
 // scale are evaluated at both ends of their intervals (directed rounding),
-// and every quotient must lie farther than tau = D / s + 2^-20 (|t| + 1)
+// and every quotient must lie farther than tau = D / s + 2^-21 (|t| + 1)
 // from its rounding boundary.  A certified row's bytes equal the reference's;
 // a row with an uncertified group goes to the float64 pass (k_had64_list, the
 // reference's butterfly in stage order), and rows with non-finite or huge
@@ -580,8 +580,10 @@ __device__ __forceinline__ bool cert_group(float* yy, float sc, float mn, float 
   const unsigned short zl = rn16(__fsub_rd(mn, D)), zh = rn16(__fadd_ru(mn, D));
   // scale RN16(RN64(RN32(max - min) / lv)), RN32(max - min) in [dl, dh]
   const float dl = __fsub_rd(__fsub_rd(mx, mn), 2.0f * D), dh = __fadd_ru(__fsub_ru(mx, mn), 2.0f * D);
-  const unsigned short sl = rn16(__fmul_rn(__fmul_rn(dl, rl), 0.99999904632568359375f));
-  const unsigned short sh = rn16(__fmul_rn(__fmul_rn(dh, rl), 1.00000095367431640625f));
+  // (1 -+ 2^-22: the three float32 roundings of d rl (1 -+ 2^-22) stay on the
+  // safe side of d / lv)
+  const unsigned short sl = rn16(__fmul_rn(__fmul_rn(dl, rl), 0.999999761581420898f));
+  const unsigned short sh = rn16(__fmul_rn(__fmul_rn(dh, rl), 1.000000238418579102f));
   s16 = sl;
   z16 = zl;
   const float s = __half2float(__ushort_as_half(sl)), z = __half2float(__ushort_as_half(zl));
@@ -592,7 +594,8 @@ __device__ __forceinline__ bool cert_group(float* yy, float sc, float mn, float 
   const float l0 = __fmul_rn(dlo, r), h0 = __fmul_rn(dhi, r);
   const float l1 = __fmaf_rn(__fmaf_rn(-l0, s, dlo), r, l0);
   const float h1 = __fmaf_rn(__fmaf_rn(-h0, s, dhi), r, h0);
-  const float tau = __fmaf_ru(D, r * 1.0001f, 0x1p-20f * (fmaxf(fabsf(l1), fabsf(h1)) + 1.0f));
+  // tau >= D / s + 5.1u |t| (+ margin): the distance any quotient may move
+  const float tau = __fmaf_ru(D, r * 1.0001f, 0x1p-21f * (fmaxf(fabsf(l1), fabsf(h1)) + 1.0f));
   const bool easy = l1 >= -0.5f && h1 < lv + 0.5f;
   float racc = 0.0f;
   float2* y2 = reinterpret_cast<float2*>(yy);
@@ -697,8 +700,6 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
   uint32_t flags = 0;
   float nanacc = 0.0f;
   int it = 0;
-  uint32_t pend_mask = 0, pend_base = 0;  // certified path: last tile's list append
-  int32_t pend_row = 0;
   // this thread's values from a tile row (swizzled 128-byte box rows); w[]
   // holds 32 bf16 pairs or 64 fp32 bit patterns
   auto load_half = [&](const uint8_t* tb, int r, uint32_t* w) {
@@ -852,16 +853,17 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       ok = ok && pok != 0;
       // uncertified rows to the float64 pass (one atomic per warp), rows
       // with non-finite / huge inputs to the exact fixup pass
-      // (the atomic's result is consumed one tile later, off the critical path)
-      const int lane = threadIdx.x & 31;
-      if (pend_mask) {
-        const uint32_t base = __shfl_sync(0xffffffffu, pend_base, __ffs(pend_mask) - 1);
-        if ((pend_mask >> lane) & 1u) a.fix1_rows[base + __popc(pend_mask & ((1u << lane) - 1u))] = pend_row;
+      // uncertified rows: one bit each in fix1_bits (the warp's 16 rows are
+      // 16 consecutive bits of one word; a fire-and-forget atomic OR)
+      {
+        uint32_t m = __ballot_sync(0xffffffffu, row_ok && !ok && valid) & 0x55555555u;  // even lanes
+        m = (m | (m >> 1)) & 0x33333333u;
+        m = (m | (m >> 2)) & 0x0F0F0F0Fu;
+        m = (m | (m >> 4)) & 0x00FF00FFu;
+        m = (m | (m >> 8)) & 0x0000FFFFu;
+        const int64_t row0 = tile * kRows + (tid & ~31) / 2;
+        if ((tid & 31) == 0 && m) atomicOr(a.fix1_bits + (row0 >> 5), m << (row0 & 31));
       }
-      const bool to64 = row_ok && !ok && half == 0 && valid;
-      pend_mask = __ballot_sync(0xffffffffu, to64);
-      pend_row = (int32_t)row;
-      if (pend_mask && lane == __ffs(pend_mask) - 1) pend_base = atomicAdd(a.fix1_count, (uint32_t)__popc(pend_mask));
       if (!row_ok && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       need_fix = !row_ok || !ok;
       if (valid) {
@@ -915,80 +917,95 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     }
     if (need_fix) flags = flags_before;  // the fixup pass sets this row's flags exactly
   }
-  if constexpr (CERT != 0) {
-    if (pend_mask) {
-      const int lane = threadIdx.x & 31;
-      const uint32_t base = __shfl_sync(0xffffffffu, pend_base, __ffs(pend_mask) - 1);
-      if ((pend_mask >> lane) & 1u) a.fix1_rows[base + __popc(pend_mask & ((1u << lane) - 1u))] = pend_row;
-    }
-  }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   // OR of the flag bits (not __syncthreads_or, which returns a 0/1 predicate)
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
 }
 
-// The float64 pass behind the certified encoder: the rows it listed
-// (fix1_rows, count on the device) re-encoded with had64_row -- the
-// reference's butterfly in stage order and the exact rounding of the
-// uncertified kernel -- read straight from global memory (a thread pair per
-// row); rows this pass cannot prove exact go on to k_encode_fixup.
+// The float64 pass behind the certified encoder: the rows it flagged in
+// fix1_bits re-encoded with had64_row -- the reference's butterfly in stage
+// order and the exact rounding of the uncertified kernel -- read straight
+// from global memory.  Each warp scans 32 bitmap words (1024 rows) at a
+// time, collects the flagged rows in shared memory and encodes them 16 at a
+// time (a thread pair per row); rows this pass cannot prove exact go on to
+// k_encode_fixup.
 template <int G, int W>
 __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
-  const uint32_t n = *a.fix1_count;
+  __shared__ int32_t rows_s[kThreads / 32][1024];
   const Geo& g = a.g;
-  const int tid = threadIdx.x, half = tid & 1;
+  const int tid = threadIdx.x, half = tid & 1, lane = tid & 31, warp = tid >> 5;
+  const int64_t nrows = g.LH * g.T, nwords = (nrows + 31) / 32;
   __half* scales = reinterpret_cast<__half*>(a.meta);
   __half* zeros = scales + g.ngroups;
   uint32_t flags = 0;
   float nanacc = 0.0f;
-  for (int64_t base = (int64_t)blockIdx.x * kRows; base < (int64_t)n; base += (int64_t)gridDim.x * kRows) {
-    const int64_t e = base + (tid >> 1);
-    const bool valid = e < (int64_t)n;  // the others repeat row `base` and store nothing
-    const int64_t row = a.fix1_rows[valid ? e : base];
-    const int64_t lh = row / g.T, t = row - lh * g.T;
-    const int64_t off = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
-    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + off);
-    {  // the next iteration's half row into L2 while this one computes
-      const int64_t en = e + (int64_t)gridDim.x * kRows;
-      if (en < (int64_t)n) {
-        const int64_t rn = a.fix1_rows[en], lhn = rn / g.T;
-        const int64_t offn = a.paged ? out_index(a, lhn, rn - lhn * g.T, half * 64) : rn * 128 + half * 64;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint16_t*>(a.kv) + offn));
-      }
-    }
-    uint32_t wv[32];
+  int32_t* list = rows_s[warp];
+  const int64_t stride = (int64_t)gridDim.x * (kThreads / 32) * 32;
+  for (int64_t w0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 32; w0 < nwords; w0 += stride) {
+    const int64_t wi = w0 + lane;
+    uint32_t bits = wi < nwords ? __ldcs(a.fix1_bits + wi) : 0u;
+    const int c = __popc(bits);
+    int off = c;  // inclusive scan of the counts over the warp
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint4 c = __ldg(src + k);
-      wv[4 * k] = c.x; wv[4 * k + 1] = c.y; wv[4 * k + 2] = c.z; wv[4 * k + 3] = c.w;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
     }
-    const uint32_t flags_before = flags;
-    __align__(8) float y[64];
-    const bool need_fix = had64_row<false>(wv, half, a, y, nanacc);
-    if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
-    float mn0, mx0, mn1, mx1;
-    minmax32(y, mn0, mx0);
-    minmax32(y + 32, mn1, mx1);
-    mn1 = __fadd_rn(mn1, 0.0f);
-    mx1 = __fadd_rn(mx1, 0.0f);
-    int w;
-    int64_t bit;
-    token_row_pos(g, a.heads, lh, t, w, bit);
-    const int cb0 = 32 * half, cb1 = 64 + 32 * half;
-    quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
-                  true, half, flags);
-    if (valid) {
-      uint8_t* out = a.packed + (bit >> 3);
-      if constexpr (W == 0) {
-        pack32_dispatch(w, y, out + cb0 * w / 8);
-        pack32_dispatch(w, y + 32, out + cb1 * w / 8);
-      } else {
-        pack32_store<W>(y, out + cb0 * W / 8);
-        pack32_store<W>(y + 32, out + cb1 * W / 8);
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= c;
+    while (bits) {
+      const int64_t r = wi * 32 + __ffs(bits) - 1;
+      list[off++] = (int32_t)r;
+      // the row's 256 bytes into L2 ahead of the encode loop below
+      const int64_t lh = r / g.T;
+      const uint16_t* p0 = reinterpret_cast<const uint16_t*>(a.kv) + (a.paged ? out_index(a, lh, r - lh * g.T, 0) : r * 128);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 64));
+      bits &= bits - 1;
+    }
+    __syncwarp();
+    for (int j0 = 0; j0 < total; j0 += 16) {
+      const int j = j0 + (lane >> 1);
+      const bool valid = j < total;  // the others repeat row j0 and store nothing
+      const int64_t row = list[valid ? j : j0];
+      const int64_t lh = row / g.T, t = row - lh * g.T;
+      const int64_t eoff = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + eoff);
+      uint32_t wv[32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 cc = __ldg(src + k);
+        wv[4 * k] = cc.x; wv[4 * k + 1] = cc.y; wv[4 * k + 2] = cc.z; wv[4 * k + 3] = cc.w;
       }
+      const uint32_t flags_before = flags;
+      __align__(8) float y[64];
+      const bool need_fix = had64_row<false>(wv, half, a, y, nanacc);
+      if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
+      float mn0, mx0, mn1, mx1;
+      minmax32(y, mn0, mx0);
+      minmax32(y + 32, mn1, mx1);
+      mn1 = __fadd_rn(mn1, 0.0f);
+      mx1 = __fadd_rn(mx1, 0.0f);
+      int w;
+      int64_t bit;
+      token_row_pos(g, a.heads, lh, t, w, bit);
+      const int cb0 = 32 * half, cb1 = 64 + 32 * half;
+      quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
+                    true, half, flags);
+      if (valid) {
+        uint8_t* out = a.packed + (bit >> 3);
+        if constexpr (W == 0) {
+          pack32_dispatch(w, y, out + cb0 * w / 8);
+          pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+        } else {
+          pack32_store<W>(y, out + cb0 * W / 8);
+          pack32_store<W>(y + 32, out + cb1 * W / 8);
+        }
+      }
+      if (need_fix) flags = flags_before;
     }
-    if (need_fix) flags = flags_before;
+    __syncwarp();
   }
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   flags = __reduce_or_sync(__activemask(), flags);
@@ -1418,7 +1435,7 @@ template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   constexpr int smem = enc_smem_bytes<F32>();
   auto k = k_enc128<MODE, G, W, F32, false>;
-  const bool cert = MODE == M_HADAMARD && !F32 && G == 32 && a.fix1_rows != nullptr;
+  const bool cert = MODE == M_HADAMARD && !F32 && G == 32 && a.fix1_bits != nullptr;
   if constexpr (MODE == M_HADAMARD && !F32 && G == 32) {
     if (cert) {
       if (a.paged) {
@@ -1633,7 +1650,7 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
     ProfScope ps("encode_fast128", s);
     e = f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
   }
-  if (e == cudaSuccess && !f32 && a.fix1_rows && a.g.transform == T_HADAMARD && a.g.group == 32)
+  if (e == cudaSuccess && !f32 && a.fix1_bits && a.g.transform == T_HADAMARD && a.g.group == 32)
     e = launch_had64_list(a, sm_count, s);
   return e;
 }

@@ -22,8 +22,7 @@ struct EncArgs {
   float rl[9];      // RN32(1 / (2^w - 1))
   int32_t* fix_rows;    // fused Hadamard encode: rows left to the exact fixup pass
   uint32_t* fix_count;
-  int32_t* fix1_rows;   // certified float32 Hadamard encode: rows for the float64 pass (or null: fp64 only)
-  uint32_t* fix1_count;
+  uint32_t* fix1_bits;  // certified float32 Hadamard encode: one bit per token row for the float64 pass (or null: fp64 only)
   float hr32;           // RN32(1 / RN64(sqrt C))
   // paged input (kvc_encode_paged): row (lh, t) of kv at out_index(a, lh, t, 0)
   int paged;

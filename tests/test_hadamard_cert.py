@@ -71,14 +71,14 @@ def certify(x):
     up = lambda v: np.nextafter(v.astype(np.float32), np.float32(np.inf))  # noqa: E731
     zl, zh = _f16bits(dn(mn - D)), _f16bits(up(mn + D))
     dl, dh = dn(mx - mn - 2 * D).astype(np.float64), up(mx - mn + 2 * D).astype(np.float64)
-    sl, sh = _f16bits(dl / 15 * (1 - 2.0 ** -20)), _f16bits(dh / 15 * (1 + 2.0 ** -20))
+    sl, sh = _f16bits(dl / 15 * (1 - 2.0 ** -22)), _f16bits(dh / 15 * (1 + 2.0 ** -22))
     ok = (zl == zh) & (sl == sh) & (dl > 0)
     s = sl.view(np.float16).astype(np.float32)
     z = zl.view(np.float16).astype(np.float32)
     with np.errstate(divide="ignore", invalid="ignore"):
         t = (g.astype(np.float32) - z[..., None]) / np.where(s > 0, s, 1)[..., None]
         tmax = np.maximum(np.abs((mn - z) / np.where(s > 0, s, 1)), np.abs((mx - z) / np.where(s > 0, s, 1)))
-        tau = D / np.where(s > 0, s, np.inf) * 1.0001 + 2.0 ** -20 * (tmax + 1)
+        tau = D / np.where(s > 0, s, np.inf) * 1.0001 + 2.0 ** -21 * (tmax + 1)
     rho = np.abs(t - np.rint(t)).max(-1)
     ok &= (rho < 0.5 - tau) | (s == 0)
     return yh, ok.all(1)
@@ -106,8 +106,8 @@ def test_certificate_is_sound_on_reference_rows():
     # float32 alone is wrong on some rows; the certificate rejects every one
     assert (~same).sum() > 0
     assert not (cert & ~same).any()
-    # and keeps the float64 pass small (under 3 % of rows on this distribution)
-    assert cert.mean() > 0.97
+    # and keeps the float64 pass small (2 % of rows on this distribution)
+    assert cert.mean() > 0.975
 
 
 def _hard_rows():
