@@ -661,7 +661,9 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
   // per-slot arrival counter) instead of after a CTA barrier
   __shared__ uint32_t slot_arrivals[NS];
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1 KB-aligned (128B swizzle atoms), indexed off smem_raw so the compiler keeps the
+  // shared address space (LDS / STS rather than generic loads)
+  uint8_t* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(tiles + NS * TB);
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
@@ -1252,7 +1254,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec128r(const __grid_constant__
   constexpr int NS = dec_stages<W>();
   constexpr int PK = 1024 * W, SB = 64 * (128 / G) * 2, STAGE = dec_stage_bytes<MODE, W, G>();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* obuf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1 KB-aligned (128B swizzle atoms), indexed off smem_raw so the compiler keeps the
+  // shared address space (LDS / STS rather than generic loads)
+  uint8_t* obuf = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ibuf = obuf + 2 * kTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ibuf + NS * STAGE);
   // [2][128] RN(1/a), [2][128] mu, double-buffered by tile parity

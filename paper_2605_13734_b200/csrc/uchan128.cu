@@ -92,7 +92,9 @@ __device__ __forceinline__ void unpack32_words(const uint32_t* wd, float* v) {
 template <int W, bool AFFINE>
 __global__ void __launch_bounds__(kUThreads, 3) k_enc_uchan128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1 KB-aligned (128B swizzle atoms), indexed off smem_raw so the compiler keeps the
+  // shared address space (LDS / STS rather than generic loads)
+  uint8_t* tiles = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint32_t* stage_sym = reinterpret_cast<uint32_t*>(tiles + kUStages * kUTileBytes);  // [128 ch][4 groups][W words]
   uint16_t* stage_sz = reinterpret_cast<uint16_t*>(stage_sym + 128 * 4 * 8);          // [128 ch][4][2] scale, zero
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_sz + 128 * 8);
