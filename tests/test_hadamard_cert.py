@@ -147,3 +147,55 @@ def test_gpu_certified_encoder_on_hard_rows(sid):
     codec.check()
     assert blob.metadata_bytes() == ref["metadata"]
     assert blob.payload_bytes() == ref["payload"]
+
+
+def _stress_rows(seed, n=8192):
+    """bf16 rows from distributions unlike the reference generator: heavy
+    tails, integer grids (exact zero outputs, ties, degenerate groups), wide
+    exponent spans, tiny / subnormal magnitudes, near-constant rows."""
+    rng = np.random.default_rng(seed)
+    k = n // 8
+    parts = [
+        rng.standard_cauchy((k, 128)).clip(-1e3, 1e3),                      # heavy tails
+        rng.integers(-8, 9, (k, 128)).astype(np.float64),                   # integer grid
+        rng.normal(size=(k, 128)) * 2.0 ** rng.integers(-30, 30, (k, 1)),   # row scales
+        rng.normal(size=(k, 128)) * 2.0 ** rng.integers(-40, 20, (k, 128)),  # per-value exponent spread
+        rng.normal(size=(k, 128)) * 1e-38,                                  # float32 subnormal range
+        1.0 + rng.normal(size=(k, 128)) * 2.0 ** -9,                        # near-constant rows
+        rng.uniform(-1, 1, (k, 128)) * (rng.uniform(size=(k, 128)) < 0.1),   # sparse
+        rng.lognormal(0, 2, (k, 128)) * rng.choice([-1.0, 1.0], (k, 128)),  # log-normal magnitudes
+    ]
+    x = np.concatenate(parts).astype(np.float32)
+    return _bf16(x)[rng.permutation(len(x))]
+
+
+def test_certificate_is_sound_on_stress_rows():
+    x = _stress_rows(7)
+    yref = (oracle.fwht64(x) / C).astype(np.float32)
+    yh, cert = certify(x)
+    with np.errstate(all="ignore"):
+        a, b = _quant(yref), _quant(yh)
+    same = np.ones(x.shape[0], bool)
+    for p, q in zip(a, b):
+        same &= (p == q).all(1)
+    assert not (cert & ~same).any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [1, 2])
+def test_gpu_certified_encoder_on_stress_rows(seed):
+    import torch
+
+    from paper_2605_13734_b200 import KVCodec
+
+    sid = "t=hadamard;q=uniform,b=4,g=32;c=none"
+    rows = _stress_rows(seed)
+    shape = (4, 2, rows.shape[0] // 8, 128)
+    vb = rows.reshape(shape)
+    with np.errstate(all="ignore"):
+        ref = oracle.encode_blob(vb, None, sid, block=256)
+    codec = KVCodec(sid, shape, block_symbols=256)
+    blob = codec.encode(torch.from_numpy(vb).to(torch.bfloat16).cuda())
+    codec.check()
+    assert blob.metadata_bytes() == ref["metadata"]
+    assert blob.payload_bytes() == ref["payload"]
