@@ -731,8 +731,11 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     load_half(tb, tid, wv);
     const int64_t row = tile * kRows + (tid >> 1);
     const bool valid = row < nrows;
-    const int64_t lh = valid ? row / g.T : 0;
-    const int64_t t = valid ? row - lh * g.T : 0;
+    // (layer*head, token) of the row: not needed for uniform compile-time
+    // widths (the row's stream bit is row * 128 * W) outside delta / affine
+    constexpr bool kNeedLH = W == 0 || MODE == M_DELTA || MODE == M_AFFINE;
+    const int64_t lh = (kNeedLH && valid) ? row / g.T : 0;
+    const int64_t t = (kNeedLH && valid) ? row - lh * g.T : 0;
     uint32_t pv[NW];  // delta: previous row's half
     if (MODE == M_DELTA) {
       if (tid >= 2) {
@@ -841,7 +844,12 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       mx1 = __fadd_rn(__fmul_rn(half ? sn1 : sx1, sc1), 0.0f);
       int w;
       int64_t bit;
-      token_row_pos(g, a.heads, lh, t, w, bit);
+      if constexpr (W != 0) {
+        w = W;
+        bit = row * (128 * W);
+      } else {
+        token_row_pos(g, a.heads, lh, t, w, bit);
+      }
       unsigned short s0, z0, s1, z1;
       bool ok = cert_group(y, sc0, mn0, mx0, Dcert, w, a.rl[w], s0, z0);
       ok = cert_group(y + 32, sc1, mn1, mx1, Dcert, w, a.rl[w], s1, z1) && ok;
@@ -904,7 +912,12 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
 
     int w;
     int64_t bit;
-    token_row_pos(g, a.heads, lh, t, w, bit);
+    if constexpr (W != 0) {
+        w = W;
+        bit = row * (128 * W);
+      } else {
+        token_row_pos(g, a.heads, lh, t, w, bit);
+      }
     quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
                   hadlayout, half, flags);
     if (valid) {
