@@ -450,7 +450,7 @@ __device__ __forceinline__ bool had64_row(const uint32_t* wv, int half, const En
 // RN16(RN64(RN32(max y - min y) / levels)) and each symbol
 // clip(rint(RN32(RN32(y - z) / s))).  So the butterfly runs in float32 (two
 // values per FADD2) with a rigorous bound |y_hat - y| <= D on every output:
-//   D = ((7 - kex) + 3.01) u Sum|x| / c + 2^-140,        u = 2^-24.
+//   D = 9.3 u Sum|x| / c + 2^-140 (u = 2^-24), or 2.3u |y| when exact.
 // bf16 inputs are multiples of 2^(emin-7) below 2^(emax+1), so the partial
 // sums of the first kex = clamp(16 - (emax - emin), 0, 7) stages fit 24 bits
 // and are exact (in any stage order); the other 7 - kex stages add at most
@@ -492,7 +492,7 @@ __device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushor
 // S (chunk 0: channels 32*half.., chunk 1: 64 + 32*half.., the same layout
 // as had64_row; B's chunk 1 negated).  Returns the
 // row's bound D, or -1 when every stage was exact (the caller then bounds
-// each group by 3.01 u max|y| of that group: only the scaling and the
+// each group by 2.3u |y| of its extremes: only the scaling and the
 // reference's roundings remain).  row_ok: finite inputs with Sum|x| < 2^100
 // (no float32 overflow anywhere in the butterfly).
 __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc,
@@ -561,9 +561,10 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
   const int emin = (int)(__float_as_uint(amn) >> 23);
   const int es1 = (int)(__float_as_uint(s1 * 1.0000153f) >> 23);  // s1 (1 + 2^-16) >= Sum|x|
   if (es1 <= emin + 16) return -1.0f;
-  // 10.01 u / c, rounded up generously (1.002 covers the float32 evaluation
-  // of Sum|x| and of this coefficient)
-  return __fmaf_ru(s1, 10.01f * 0x1p-24f * a.hr32 * 1.002f, 0x1p-140f);
+  // (7 + 2.3) u / c: gamma_7 Sum|x| for the butterfly, 2.29u |S| / c for the
+  // two float32 scalings and the reference's rounding; 1.002 covers the
+  // float32 evaluation of Sum|x| and of this coefficient
+  return __fmaf_ru(s1, 9.3f * 0x1p-24f * a.hr32 * 1.002f, 0x1p-140f);
 }
 
 // Quantize one certified group of 32 unscaled sums (y = S sc, sc = +-RN32(1/c);
@@ -574,12 +575,22 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
 __device__ __forceinline__ bool cert_group(float* yy, float sc, float mn, float mx, float D, int w, float rl,
                                            unsigned short& s16, unsigned short& z16) {
   const float lv = (float)((1 << w) - 1);
-  // exact butterfly: |y_hat - y| <= 3.01 u |S_j| / c <= 3.01 u max|y_hat| (1 + 2.1u) of the group
-  if (D < 0.0f) D = __fmaf_ru(fmaxf(fabsf(mn), fabsf(mx)), 3.02f * 0x1p-24f, 0x1p-140f);
-  // zero RN16(min y), min y in [mn - D, mn + D]
-  const unsigned short zl = rn16(__fsub_rd(mn, D)), zh = rn16(__fadd_ru(mn, D));
+  // exact butterfly: each output is off by at most 2.29u |y| (RN32 of S
+  // RN32(1/c), whose error is 0.287u, and the reference's own RN32): the
+  // group's min within 2.3u |mn|, its max within 2.3u |mx| (the bound of the
+  // extreme element bounds every element beyond it), any value within
+  // 2.3u max(|mn|, |mx|)
+  float Dz = D, Dx = D;
+  if (D < 0.0f) {
+    Dz = __fmaf_ru(fabsf(mn), 2.3f * 0x1p-24f, 0x1p-140f);
+    Dx = __fmaf_ru(fabsf(mx), 2.3f * 0x1p-24f, 0x1p-140f);
+    D = fmaxf(Dz, Dx);
+  }
+  // zero RN16(min y), min y in [mn - Dz, mn + Dz]
+  const unsigned short zl = rn16(__fsub_rd(mn, Dz)), zh = rn16(__fadd_ru(mn, Dz));
   // scale RN16(RN64(RN32(max - min) / lv)), RN32(max - min) in [dl, dh]
-  const float dl = __fsub_rd(__fsub_rd(mx, mn), 2.0f * D), dh = __fadd_ru(__fsub_ru(mx, mn), 2.0f * D);
+  const float Dd = __fadd_ru(Dz, Dx);
+  const float dl = __fsub_rd(__fsub_rd(mx, mn), Dd), dh = __fadd_ru(__fsub_ru(mx, mn), Dd);
   // (1 -+ 2^-22: the three float32 roundings of d rl (1 -+ 2^-22) stay on the
   // safe side of d / lv)
   const unsigned short sl = rn16(__fmul_rn(__fmul_rn(dl, rl), 0.999999761581420898f));

@@ -64,13 +64,15 @@ def certify(x):
     exact = es1 <= emin + 16
     g = yh.reshape(N, 4, 32).astype(np.float64)
     mn, mx = g.min(-1), g.max(-1)
-    d_sum = (10.01 * U * s1 / C * 1.002 + 2.0 ** -140)[:, None]
-    d_exact = 3.02 * U * np.maximum(np.abs(mn), np.abs(mx)) + 2.0 ** -140
-    D = np.where(exact[:, None], d_exact, d_sum)
+    d_sum = (9.3 * U * s1 / C * 1.002 + 2.0 ** -140)[:, None]
+    ex = exact[:, None]
+    dz = np.where(ex, 2.3 * U * np.abs(mn) + 2.0 ** -140, d_sum)
+    dx = np.where(ex, 2.3 * U * np.abs(mx) + 2.0 ** -140, d_sum)
+    D = np.maximum(dz, dx)
     dn = lambda v: np.nextafter(v.astype(np.float32), np.float32(-np.inf))  # noqa: E731
     up = lambda v: np.nextafter(v.astype(np.float32), np.float32(np.inf))  # noqa: E731
-    zl, zh = _f16bits(dn(mn - D)), _f16bits(up(mn + D))
-    dl, dh = dn(mx - mn - 2 * D).astype(np.float64), up(mx - mn + 2 * D).astype(np.float64)
+    zl, zh = _f16bits(dn(mn - dz)), _f16bits(up(mn + dz))
+    dl, dh = dn(mx - mn - (dz + dx)).astype(np.float64), up(mx - mn + (dz + dx)).astype(np.float64)
     sl, sh = _f16bits(dl / 15 * (1 - 2.0 ** -22)), _f16bits(dh / 15 * (1 + 2.0 ** -22))
     ok = (zl == zh) & (sl == sh) & (dl > 0)
     s = sl.view(np.float16).astype(np.float32)
