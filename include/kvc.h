@@ -81,7 +81,7 @@ int kvc_plan_destroy(kvc_plan* plan);
 const char* kvc_plan_strategy_id(const kvc_plan* plan);
 
 /* Kernel family kvc_encode / kvc_decode run for this plan: "fast128",
- * "fast128-cert+fp64+fixup" (Hadamard, bf16, 32-channel groups: the certified
+ * "fast128-cert+fp64+fixup" (Hadamard, bf16 input: the certified
  * float32 encoder, a float64 pass for the rows it cannot certify, then the
  * exact fixup; the environment variable KVC_HADAMARD_FP64=1 selects the
  * float64 encoder instead), "fast128+fixup", "uchan128", "fused_rc",

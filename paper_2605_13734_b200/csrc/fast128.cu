@@ -441,8 +441,9 @@ __device__ __forceinline__ bool had64_row(const uint32_t* wv, int half, const En
 }
 
 // ---------------------------------------------------------------------------
-// Certified float32 Hadamard encode (bf16 input, 32-channel groups: the
-// reference default profile, transforms.py:62 + quantize.py:142-154).
+// Certified float32 Hadamard encode (bf16 input, 32- / 64- / 128-channel
+// groups; 32 is the reference default profile, transforms.py:62 +
+// quantize.py:142-154).
 //
 // The reference's y = RN32(RN64(S / c)) (S the float64 butterfly sum,
 // c = RN64(sqrt 128)) reaches the payload only through three decisions, each
@@ -659,14 +660,14 @@ __host__ __device__ constexpr int enc_smem_bytes() {
 
 // PAGED: bf16 input read from a paged cache (5D boxes per page run); a
 // separate instantiation so the contiguous kernels keep their exact code
-// CERT: the certified float32 Hadamard (bf16, G = 32) with the float64 pass
+// CERT: the certified float32 Hadamard (bf16 input) with the float64 pass
 // behind it for the rows it cannot certify
 // (4 CTAs per SM; 5, with a 2-stage ring and 96 registers, measured the same)
 template <int MODE, int G, int W, bool F32 = false, bool PAGED = false, int CERT = 0>
 __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   static_assert(!(F32 && PAGED), "paged input is bf16");
-  static_assert(CERT == 0 || (MODE == M_HADAMARD && !F32 && G == 32), "certified path: bf16 Hadamard, 32-channel groups");
+  static_assert(CERT == 0 || (MODE == M_HADAMARD && !F32), "certified path: bf16 Hadamard");
   constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
   // certified path: a slot is refilled by the last warp to copy it out (a
   // per-slot arrival counter) instead of after a CTA barrier
@@ -853,6 +854,19 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       mx0 = __fmul_rn(sx0, sc0);
       mn1 = __fadd_rn(__fmul_rn(half ? sx1 : sn1, sc1), 0.0f);  // -0 from the negation -> +0
       mx1 = __fadd_rn(__fmul_rn(half ? sn1 : sx1, sc1), 0.0f);
+      if constexpr (G == 64) {  // group c = chunk c of both threads
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      } else if constexpr (G == 128) {  // one group per row
+        mn0 = fminf(mn0, mn1);
+        mx0 = fmaxf(mx0, mx1);
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mn1 = mn0;
+        mx1 = mx0;
+      }
       int w;
       int64_t bit;
       if constexpr (W != 0) {
@@ -864,11 +878,19 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
       unsigned short s0, z0, s1, z1;
       bool ok = cert_group(y, sc0, mn0, mx0, Dcert, w, a.rl[w], s0, z0);
       ok = cert_group(y + 32, sc1, mn1, mx1, Dcert, w, a.rl[w], s1, z1) && ok;
-      if (valid) {
-        scales[row * 4 + half] = __ushort_as_half(s0);
-        zeros[row * 4 + half] = __ushort_as_half(z0);
-        scales[row * 4 + 2 + half] = __ushort_as_half(s1);
-        zeros[row * 4 + 2 + half] = __ushort_as_half(z1);
+      if (valid) {  // one writer per group (both threads hold the same scale / zero)
+        if constexpr (G == 32) {
+          scales[row * 4 + half] = __ushort_as_half(s0);
+          zeros[row * 4 + half] = __ushort_as_half(z0);
+          scales[row * 4 + 2 + half] = __ushort_as_half(s1);
+          zeros[row * 4 + 2 + half] = __ushort_as_half(z1);
+        } else if constexpr (G == 64) {
+          scales[row * 2 + half] = __ushort_as_half(half ? s1 : s0);
+          zeros[row * 2 + half] = __ushort_as_half(half ? z1 : z0);
+        } else if (half == 0) {
+          scales[row] = __ushort_as_half(s0);
+          zeros[row] = __ushort_as_half(z0);
+        }
       }
       const int pok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);  // every lane shuffles (no short circuit)
       ok = ok && pok != 0;
@@ -1463,8 +1485,8 @@ template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   constexpr int smem = enc_smem_bytes<F32>();
   auto k = k_enc128<MODE, G, W, F32, false>;
-  const bool cert = MODE == M_HADAMARD && !F32 && G == 32 && a.fix1_bits != nullptr;
-  if constexpr (MODE == M_HADAMARD && !F32 && G == 32) {
+  const bool cert = MODE == M_HADAMARD && !F32 && a.fix1_bits != nullptr;
+  if constexpr (MODE == M_HADAMARD && !F32) {
     if (cert) {
       if (a.paged) {
         k = k_enc128<MODE, G, W, false, true, 1>;
@@ -1641,23 +1663,32 @@ bool fast128_applicable(const Geo& g) {
   return true;
 }
 
-template <int W>
-cudaError_t launch_had64_list_w(const EncArgs& a, int sm_count, cudaStream_t s) {
+template <int G, int W>
+cudaError_t launch_had64_list_gw(const EncArgs& a, int sm_count, cudaStream_t s) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had64_list<32, W>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had64_list<G, W>, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
-  k_had64_list<32, W><<<(unsigned)(sm_count * per_sm), kThreads, 0, s>>>(a);
+  k_had64_list<G, W><<<(unsigned)(sm_count * per_sm), kThreads, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t launch_had64_list_g(const EncArgs& a, int sm_count, cudaStream_t s) {
+  switch (a.g.quant == Q_UNIFORM ? a.g.bits : 0) {
+    case 2: return launch_had64_list_gw<G, 2>(a, sm_count, s);
+    case 4: return launch_had64_list_gw<G, 4>(a, sm_count, s);
+    case 8: return launch_had64_list_gw<G, 8>(a, sm_count, s);
+    default: return launch_had64_list_gw<G, 0>(a, sm_count, s);
+  }
 }
 
 // the float64 pass over the rows the certified encoder listed
 cudaError_t launch_had64_list(const EncArgs& a, int sm_count, cudaStream_t s) {
   ProfScope ps("encode_had64_list", s);
-  switch (a.g.quant == Q_UNIFORM ? a.g.bits : 0) {
-    case 2: return launch_had64_list_w<2>(a, sm_count, s);
-    case 4: return launch_had64_list_w<4>(a, sm_count, s);
-    case 8: return launch_had64_list_w<8>(a, sm_count, s);
-    default: return launch_had64_list_w<0>(a, sm_count, s);
+  switch (a.g.group) {
+    case 32: return launch_had64_list_g<32>(a, sm_count, s);
+    case 64: return launch_had64_list_g<64>(a, sm_count, s);
+    default: return launch_had64_list_g<128>(a, sm_count, s);
   }
 }
 
@@ -1678,7 +1709,7 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
     ProfScope ps("encode_fast128", s);
     e = f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
   }
-  if (e == cudaSuccess && !f32 && a.fix1_bits && a.g.transform == T_HADAMARD && a.g.group == 32)
+  if (e == cudaSuccess && !f32 && a.fix1_bits && a.g.transform == T_HADAMARD)
     e = launch_had64_list(a, sm_count, s);
   return e;
 }

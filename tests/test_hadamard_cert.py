@@ -184,13 +184,16 @@ def test_certificate_is_sound_on_stress_rows():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", [1, 2])
-def test_gpu_certified_encoder_on_stress_rows(seed):
+@pytest.mark.parametrize("seed,sid", [(1, "t=hadamard;q=uniform,b=4,g=32;c=none"),
+                                      (2, "t=hadamard;q=uniform,b=4,g=32;c=none"),
+                                      (3, "t=hadamard;q=uniform,b=2,g=64;c=none"),
+                                      (4, "t=hadamard;q=uniform,b=8,g=128;c=none"),
+                                      (5, "t=hadamard;q=uniform,b=3,g=64;c=entropy")])
+def test_gpu_certified_encoder_on_stress_rows(seed, sid):
     import torch
 
     from paper_2605_13734_b200 import KVCodec
 
-    sid = "t=hadamard;q=uniform,b=4,g=32;c=none"
     rows = _stress_rows(seed)
     shape = (4, 2, rows.shape[0] // 8, 128)
     vb = rows.reshape(shape)
