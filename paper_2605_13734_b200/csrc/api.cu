@@ -455,10 +455,10 @@ const char* kvc_plan_encode_path(const kvc_plan* plan) {
     const int64_t box_rows = (g.in_dtype == KVC_DTYPE_F32 ? 4 : 2) * g.LH * g.T;
     if (box_rows >= (1ll << 31)) return "generic: too many token rows for a 2-D tensor map";
     if (g.transform != T_HADAMARD) return "fast128";
-    // bf16: the certified float32 encoder, its float64
+    // the certified float32 encoder, its float64
     // pass and the exact fixup (KVC_HADAMARD_FP64=1: the float64 encoder)
     const char* fp64 = getenv("KVC_HADAMARD_FP64");
-    if (g.in_dtype == KVC_DTYPE_BF16 && !(fp64 && atoi(fp64) != 0)) return "fast128-cert+fp64+fixup";
+    if (!(fp64 && atoi(fp64) != 0)) return "fast128-cert+fp64+fixup";
     return "fast128+fixup";
   }
   if (uchan128_applicable(g)) {

@@ -496,17 +496,22 @@ __device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushor
 // each group by 2.3u |y| of its extremes: only the scaling and the
 // reference's roundings remain).  row_ok: finite inputs with Sum|x| < 2^100
 // (no float32 overflow anywhere in the butterfly).
+template <bool F32>
 __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc,
                                            bool& row_ok) {
   // P[m] = (local m, local m + 32): stages h = 1..16 pair P[m] with P[m + h]
   float2 P[32];
 #pragma unroll
   for (int m = 0; m < 32; ++m)
-    P[m] = make_float2(__uint_as_float(vbits_of<false>(wv, m)), __uint_as_float(vbits_of<false>(wv, m + 32)));
-  // min |x| (three per FMNMX3, |.| free): the inputs' 2^(emin-7) grid
-  float amn = fminf(fabsf(P[0].x), fabsf(P[0].y));
+    P[m] = make_float2(__uint_as_float(vbits_of<F32>(wv, m)), __uint_as_float(vbits_of<F32>(wv, m + 32)));
+  // min |x| (three per FMNMX3, |.| free): the inputs' 2^(emin-7) grid (bf16;
+  // float32 inputs carry 24-bit significands and take the gamma_7 bound)
+  float amn = 0.0f;
+  if constexpr (!F32) {
+    amn = fminf(fabsf(P[0].x), fabsf(P[0].y));
 #pragma unroll
-  for (int m = 1; m < 32; ++m) amn = min3f(amn, fabsf(P[m].x), fabsf(P[m].y));
+    for (int m = 1; m < 32; ++m) amn = min3f(amn, fabsf(P[m].x), fabsf(P[m].y));
+  }
   // h = 1, and Sum|x| as max(|a + b|, |a - b|) = |a| + |b| per pair (a NaN
   // input makes the sum NaN)
   float2 sa = make_float2(0.0f, 0.0f);
@@ -551,7 +556,7 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
   }
   float s1 = sa.x + sa.y;
   s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-  amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
+  if constexpr (!F32) amn = fminf(amn, __shfl_xor_sync(0xffffffffu, amn, 1));
   // a NaN / inf input (or a sum near the float32 range) makes s1 NaN / huge:
   // the row goes to the exact fixup pass, which also raises the input flag
   row_ok = s1 < 0x1p100f;
@@ -559,9 +564,11 @@ __device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const E
   // below 2^(es1+1) (es1: exponent of an upper bound of Sum|x|), so all
   // seven stages are exact when es1 <= emin + 16 (24 bits); other rows take
   // the gamma_7 bound
-  const int emin = (int)(__float_as_uint(amn) >> 23);
-  const int es1 = (int)(__float_as_uint(s1 * 1.0000153f) >> 23);  // s1 (1 + 2^-16) >= Sum|x|
-  if (es1 <= emin + 16) return -1.0f;
+  if constexpr (!F32) {
+    const int emin = (int)(__float_as_uint(amn) >> 23);
+    const int es1 = (int)(__float_as_uint(s1 * 1.0000153f) >> 23);  // s1 (1 + 2^-16) >= Sum|x|
+    if (es1 <= emin + 16) return -1.0f;
+  }
   // (7 + 2.3) u / c: gamma_7 Sum|x| for the butterfly, 2.29u |S| / c for the
   // two float32 scalings and the reference's rounding; 1.002 covers the
   // float32 evaluation of Sum|x| and of this coefficient
@@ -667,7 +674,7 @@ template <int MODE, int G, int W, bool F32 = false, bool PAGED = false, int CERT
 __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MODE == M_DELTA) ? 3 : 4)
     k_enc128(const __grid_constant__ CUtensorMap tmap, const EncArgs a) {
   static_assert(!(F32 && PAGED), "paged input is bf16");
-  static_assert(CERT == 0 || (MODE == M_HADAMARD && !F32), "certified path: bf16 Hadamard");
+  static_assert(CERT == 0 || MODE == M_HADAMARD, "certified path: Hadamard");
   constexpr int NS = enc_stages<F32>(), TB = enc_tile_bytes<F32>();
   // certified path: a slot is refilled by the last warp to copy it out (a
   // per-slot arrival counter) instead of after a CTA barrier
@@ -800,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     const uint32_t flags_before = flags;
     if (MODE == M_HADAMARD) {
       if constexpr (CERT) {
-        Dcert = had32_row(wv, half, a, y, nanacc, row_ok);
+        Dcert = had32_row<F32>(wv, half, a, y, nanacc, row_ok);
       } else {
         need_fix = had64_row<F32>(wv, half, a, y, nanacc);
         if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
@@ -978,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
 // time, collects the flagged rows in shared memory and encodes them 16 at a
 // time (a thread pair per row); rows this pass cannot prove exact go on to
 // k_encode_fixup.
-template <int G, int W>
+template <int G, int W, bool F32>
 __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
   __shared__ int32_t rows_s[kThreads / 32][1024];
   const Geo& g = a.g;
@@ -1007,9 +1014,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
       list[off++] = (int32_t)r;
       // the row's 256 bytes into L2 ahead of the encode loop below
       const int64_t lh = r / g.T;
-      const uint16_t* p0 = reinterpret_cast<const uint16_t*>(a.kv) + (a.paged ? out_index(a, lh, r - lh * g.T, 0) : r * 128);
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 64));
+      const uint8_t* p0 = reinterpret_cast<const uint8_t*>(a.kv) +
+                          (a.paged ? out_index(a, lh, r - lh * g.T, 0) : r * 128) * (F32 ? 4 : 2);
+#pragma unroll
+      for (int q = 0; q < (F32 ? 4 : 2); ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 128 * q));
       bits &= bits - 1;
     }
     __syncwarp();
@@ -1019,16 +1027,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
       const int64_t row = list[valid ? j : j0];
       const int64_t lh = row / g.T, t = row - lh * g.T;
       const int64_t eoff = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
-      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.kv) + eoff);
-      uint32_t wv[32];
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) + eoff * (F32 ? 4 : 2));
+      constexpr int NW = F32 ? 64 : 32;
+      uint32_t wv[NW];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < NW / 4; ++k) {
         const uint4 cc = __ldg(src + k);
         wv[4 * k] = cc.x; wv[4 * k + 1] = cc.y; wv[4 * k + 2] = cc.z; wv[4 * k + 3] = cc.w;
       }
       const uint32_t flags_before = flags;
       __align__(8) float y[64];
-      const bool need_fix = had64_row<false>(wv, half, a, y, nanacc);
+      const bool need_fix = had64_row<F32>(wv, half, a, y, nanacc);
       if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
       float mn0, mx0, mn1, mx1;
       minmax32(y, mn0, mx0);
@@ -1485,10 +1494,13 @@ template <int MODE, int G, int W, bool F32>
 cudaError_t launch_enc(const CUtensorMap& map, const EncArgs& a, int sm_count, cudaStream_t s) {
   constexpr int smem = enc_smem_bytes<F32>();
   auto k = k_enc128<MODE, G, W, F32, false>;
-  const bool cert = MODE == M_HADAMARD && !F32 && a.fix1_bits != nullptr;
-  if constexpr (MODE == M_HADAMARD && !F32) {
+  const bool cert = MODE == M_HADAMARD && a.fix1_bits != nullptr;
+  if constexpr (MODE == M_HADAMARD) {
     if (cert) {
-      if (a.paged) {
+      if constexpr (F32) {
+        k = k_enc128<MODE, G, W, true, false, 1>;
+        set_max_dyn_smem<k_enc128<MODE, G, W, true, false, 1>>(smem);
+      } else if (a.paged) {
         k = k_enc128<MODE, G, W, false, true, 1>;
         set_max_dyn_smem<k_enc128<MODE, G, W, false, true, 1>>(smem);
       } else {
@@ -1665,10 +1677,11 @@ bool fast128_applicable(const Geo& g) {
 
 template <int G, int W>
 cudaError_t launch_had64_list_gw(const EncArgs& a, int sm_count, cudaStream_t s) {
+  auto k = a.g.in_dtype == KVC_DTYPE_F32 ? k_had64_list<G, W, true> : k_had64_list<G, W, false>;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_had64_list<G, W>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
-  k_had64_list<G, W><<<(unsigned)(sm_count * per_sm), kThreads, 0, s>>>(a);
+  k<<<(unsigned)(sm_count * per_sm), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1709,8 +1722,7 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
     ProfScope ps("encode_fast128", s);
     e = f32 ? launch_enc_t<true>(map, a, sm_count, s) : launch_enc_t<false>(map, a, sm_count, s);
   }
-  if (e == cudaSuccess && !f32 && a.fix1_bits && a.g.transform == T_HADAMARD)
-    e = launch_had64_list(a, sm_count, s);
+  if (e == cudaSuccess && a.fix1_bits && a.g.transform == T_HADAMARD) e = launch_had64_list(a, sm_count, s);
   return e;
 }
 

@@ -103,8 +103,8 @@ def _plan_dtype(lib, sid, in_dtype, shape=(2, 4, 64, 128), block=2048):
 
 
 @pytest.mark.parametrize("sid,bf16_path,f32_path", [
-    ("t=hadamard;q=uniform,b=4,g=32;c=none", "fast128-cert+fp64+fixup", "fast128+fixup"),
-    ("t=hadamard;q=uniform,b=4,g=64;c=none", "fast128-cert+fp64+fixup", "fast128+fixup"),
+    ("t=hadamard;q=uniform,b=4,g=32;c=none", "fast128-cert+fp64+fixup", "fast128-cert+fp64+fixup"),
+    ("t=hadamard;q=uniform,b=4,g=64;c=none", "fast128-cert+fp64+fixup", "fast128-cert+fp64+fixup"),
     ("t=identity;q=uniform,b=2,g=32;c=entropy", "fused_rc", "fast128"),
     ("t=identity;q=uchan,b=2,g=32;c=entropy", "fused_rc", "generic"),
     ("t=identity;q=uchan,b=2,g=32;c=none", "uchan128", "generic"),

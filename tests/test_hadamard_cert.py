@@ -204,3 +204,27 @@ def test_gpu_certified_encoder_on_stress_rows(seed, sid):
     codec.check()
     assert blob.metadata_bytes() == ref["metadata"]
     assert blob.payload_bytes() == ref["payload"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sid", ["t=hadamard;q=uniform,b=4,g=32;c=none", "t=hadamard;q=uniform,b=2,g=128;c=entropy"])
+def test_gpu_certified_encoder_float32_input(sid):
+    """float32 inputs (the reference's own corpora, tensors.py:79-112): no
+    exact-butterfly shortcut, every row on the gamma_7 bound; reference
+    generator rows plus the stress rows, bit-exact against the oracle."""
+    import torch
+
+    from paper_2605_13734_b200 import KVCodec
+
+    vals, _ = oracle.generate_kv(2, 4, 1024, 128, seed=11)
+    rows = np.concatenate([vals.reshape(-1, 128), _stress_rows(12, 4096) * np.float32(1.0 + 2.0 ** -12)])
+    shape = (4, 2, rows.shape[0] // 8, 128)
+    vb = np.ascontiguousarray(rows.reshape(shape), dtype=np.float32)
+    with np.errstate(all="ignore"):
+        ref = oracle.encode_blob(vb, None, sid, block=256)
+    codec = KVCodec(sid, shape, in_dtype=torch.float32, block_symbols=256)
+    blob = codec.encode(torch.from_numpy(vb).cuda())
+    codec.check()
+    assert codec.encode_path == "fast128-cert+fp64+fixup"
+    assert blob.metadata_bytes() == ref["metadata"]
+    assert blob.payload_bytes() == ref["payload"]
