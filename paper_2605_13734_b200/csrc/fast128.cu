@@ -497,8 +497,7 @@ __device__ __forceinline__ unsigned short rn16(float v) { return __half_as_ushor
 // reference's roundings remain).  row_ok: finite inputs with Sum|x| < 2^100
 // (no float32 overflow anywhere in the butterfly).
 template <bool F32>
-__device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, float& nanacc,
-                                           bool& row_ok) {
+__device__ __forceinline__ float had32_row(const uint32_t* wv, int half, const EncArgs& a, float* y, bool& row_ok) {
   // P[m] = (local m, local m + 32): stages h = 1..16 pair P[m] with P[m + h]
   float2 P[32];
 #pragma unroll
@@ -807,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     const uint32_t flags_before = flags;
     if (MODE == M_HADAMARD) {
       if constexpr (CERT) {
-        Dcert = had32_row<F32>(wv, half, a, y, nanacc, row_ok);
+        Dcert = had32_row<F32>(wv, half, a, y, row_ok);
       } else {
         need_fix = had64_row<F32>(wv, half, a, y, nanacc);
         if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
