@@ -986,7 +986,8 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
 // k_encode_fixup.
 template <int G, int W, bool F32>
 __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
-  __shared__ int32_t rows_s[kThreads / 32][1024];
+  // per warp: rows carried over from the last window (< 16) + one window's
+  __shared__ int32_t rows_s[kThreads / 32][1024 + 16];
   const Geo& g = a.g;
   const int tid = threadIdx.x, half = tid & 1, lane = tid & 31, warp = tid >> 5;
   const int64_t nrows = g.LH * g.T, nwords = (nrows + 31) / 32;
@@ -995,7 +996,50 @@ __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
   uint32_t flags = 0;
   float nanacc = 0.0f;
   int32_t* list = rows_s[warp];
+  // encode list[j0 .. j0 + 16) (rows past `total` repeat row j0 and store nothing)
+  auto enc_batch = [&](int j0, int total) {
+    const int j = j0 + (lane >> 1);
+    const bool valid = j < total;
+    const int64_t row = list[valid ? j : j0];
+    const int64_t lh = row / g.T, t = row - lh * g.T;
+    const int64_t eoff = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) + eoff * (F32 ? 4 : 2));
+    constexpr int NW = F32 ? 64 : 32;
+    uint32_t wv[NW];
+#pragma unroll
+    for (int k = 0; k < NW / 4; ++k) {
+      const uint4 cc = __ldg(src + k);
+      wv[4 * k] = cc.x; wv[4 * k + 1] = cc.y; wv[4 * k + 2] = cc.z; wv[4 * k + 3] = cc.w;
+    }
+    const uint32_t flags_before = flags;
+    __align__(8) float y[64];
+    const bool need_fix = had64_row<F32>(wv, half, a, y, nanacc);
+    if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
+    float mn0, mx0, mn1, mx1;
+    minmax32(y, mn0, mx0);
+    minmax32(y + 32, mn1, mx1);
+    mn1 = __fadd_rn(mn1, 0.0f);
+    mx1 = __fadd_rn(mx1, 0.0f);
+    int w;
+    int64_t bit;
+    token_row_pos(g, a.heads, lh, t, w, bit);
+    const int cb0 = 32 * half, cb1 = 64 + 32 * half;
+    quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
+                  true, half, flags);
+    if (valid) {
+      uint8_t* out = a.packed + (bit >> 3);
+      if constexpr (W == 0) {
+        pack32_dispatch(w, y, out + cb0 * w / 8);
+        pack32_dispatch(w, y + 32, out + cb1 * w / 8);
+      } else {
+        pack32_store<W>(y, out + cb0 * W / 8);
+        pack32_store<W>(y + 32, out + cb1 * W / 8);
+      }
+    }
+    if (need_fix) flags = flags_before;
+  };
   const int64_t stride = (int64_t)gridDim.x * (kThreads / 32) * 32;
+  int q = 0;  // rows queued in list[0 .. q)
   for (int64_t w0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * 32; w0 < nwords; w0 += stride) {
     const int64_t wi = w0 + lane;
     uint32_t bits = wi < nwords ? __ldcs(a.fix1_bits + wi) : 0u;
@@ -1007,62 +1051,31 @@ __global__ void __launch_bounds__(kThreads, 3) k_had64_list(const EncArgs a) {
       if (lane >= d) off += v;
     }
     const int total = __shfl_sync(0xffffffffu, off, 31);
-    off -= c;
+    off += q - c;
     while (bits) {
       const int64_t r = wi * 32 + __ffs(bits) - 1;
       list[off++] = (int32_t)r;
-      // the row's 256 bytes into L2 ahead of the encode loop below
+      // the row's bytes into L2 ahead of its encode
       const int64_t lh = r / g.T;
       const uint8_t* p0 = reinterpret_cast<const uint8_t*>(a.kv) +
                           (a.paged ? out_index(a, lh, r - lh * g.T, 0) : r * 128) * (F32 ? 4 : 2);
 #pragma unroll
-      for (int q = 0; q < (F32 ? 4 : 2); ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 128 * q));
+      for (int qq = 0; qq < (F32 ? 4 : 2); ++qq) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 128 * qq));
       bits &= bits - 1;
     }
     __syncwarp();
-    for (int j0 = 0; j0 < total; j0 += 16) {
-      const int j = j0 + (lane >> 1);
-      const bool valid = j < total;  // the others repeat row j0 and store nothing
-      const int64_t row = list[valid ? j : j0];
-      const int64_t lh = row / g.T, t = row - lh * g.T;
-      const int64_t eoff = a.paged ? out_index(a, lh, t, half * 64) : row * 128 + half * 64;
-      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(a.kv) + eoff * (F32 ? 4 : 2));
-      constexpr int NW = F32 ? 64 : 32;
-      uint32_t wv[NW];
-#pragma unroll
-      for (int k = 0; k < NW / 4; ++k) {
-        const uint4 cc = __ldg(src + k);
-        wv[4 * k] = cc.x; wv[4 * k + 1] = cc.y; wv[4 * k + 2] = cc.z; wv[4 * k + 3] = cc.w;
-      }
-      const uint32_t flags_before = flags;
-      __align__(8) float y[64];
-      const bool need_fix = had64_row<F32>(wv, half, a, y, nanacc);
-      if (need_fix && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
-      float mn0, mx0, mn1, mx1;
-      minmax32(y, mn0, mx0);
-      minmax32(y + 32, mn1, mx1);
-      mn1 = __fadd_rn(mn1, 0.0f);
-      mx1 = __fadd_rn(mx1, 0.0f);
-      int w;
-      int64_t bit;
-      token_row_pos(g, a.heads, lh, t, w, bit);
-      const int cb0 = 32 * half, cb1 = 64 + 32 * half;
-      quantize64<G>(y, mn0, mx0, mn1, mx1, cb0, cb1, w, a.rl[w], row * (128 / G), valid ? scales : nullptr, zeros,
-                    true, half, flags);
-      if (valid) {
-        uint8_t* out = a.packed + (bit >> 3);
-        if constexpr (W == 0) {
-          pack32_dispatch(w, y, out + cb0 * w / 8);
-          pack32_dispatch(w, y + 32, out + cb1 * w / 8);
-        } else {
-          pack32_store<W>(y, out + cb0 * W / 8);
-          pack32_store<W>(y + 32, out + cb1 * W / 8);
-        }
-      }
-      if (need_fix) flags = flags_before;
-    }
+    q += total;
+    // full batches of 16 rows now; fewer than 16 wait for the next window
+    int j0 = 0;
+    for (; j0 + 16 <= q; j0 += 16) enc_batch(j0, q);
+    const int rem = q - j0;
+    const int32_t carry = lane < rem ? list[j0 + lane] : 0;
     __syncwarp();
+    if (lane < rem) list[lane] = carry;
+    __syncwarp();
+    q = rem;
   }
+  if (q > 0) enc_batch(0, q);
   if (nanacc != 0.0f) flags |= KVC_FLAG_NONFINITE_INPUT;
   flags = __reduce_or_sync(__activemask(), flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(a.status, flags);
