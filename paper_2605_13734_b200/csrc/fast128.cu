@@ -441,30 +441,34 @@ __device__ __forceinline__ bool had64_row(const uint32_t* wv, int half, const En
 }
 
 // ---------------------------------------------------------------------------
-// Certified float32 Hadamard encode (bf16 input, 32- / 64- / 128-channel
-// groups; 32 is the reference default profile, transforms.py:62 +
-// quantize.py:142-154).
+// Certified float32 Hadamard encode (bf16 or float32 input, 32- / 64- /
+// 128-channel groups; bf16 at 32 is the reference default profile,
+// transforms.py:62 + quantize.py:142-154).
 //
 // The reference's y = RN32(RN64(S / c)) (S the float64 butterfly sum,
 // c = RN64(sqrt 128)) reaches the payload only through three decisions, each
 // monotone in y: the fp16 zero RN16(min y), the fp16 scale
 // RN16(RN64(RN32(max y - min y) / levels)) and each symbol
 // clip(rint(RN32(RN32(y - z) / s))).  So the butterfly runs in float32 (two
-// values per FADD2) with a rigorous bound |y_hat - y| <= D on every output:
-//   D = 9.3 u Sum|x| / c + 2^-140 (u = 2^-24), or 2.3u |y| when exact.
-// bf16 inputs are multiples of 2^(emin-7) below 2^(emax+1), so the partial
-// sums of the first kex = clamp(16 - (emax - emin), 0, 7) stages fit 24 bits
-// and are exact (in any stage order); the other 7 - kex stages add at most
-// gamma_(7-kex) Sum|x| (summation tree of that depth), the scaling by
-// RN32(1/c) 2u Sum|x| / c, the reference's own roundings u Sum|x| / c, and
-// subnormal intermediates below 2^-146 in all.  A group is certified when
-// every decision is constant on [y_hat - D, y_hat + D]: the zero and the
-// scale are evaluated at both ends of their intervals (directed rounding),
-// and every quotient must lie farther than tau = D / s + 2^-21 (|t| + 1)
+// values per FADD2) with a rigorous bound on every output, u = 2^-24:
+//  * exact rows -- bf16 inputs are multiples of 2^(emin-7) and every partial
+//    sum is below 2^(es1+1) (es1: exponent of Sum|x|), so with
+//    es1 <= emin + 16 all seven stages are exact in float32 (any order); what
+//    remains is RN32 of S RN32(1/c) (RN32(1/c) is within 0.287u of 1/c) and
+//    the reference's own RN32: |y_hat - y| <= 2.3u |y|, so a group's min is
+//    within 2.3u |min|, its max within 2.3u |max|;
+//  * other rows (and float32 inputs): gamma_7 Sum|x| for any depth-7
+//    summation tree plus those roundings, D = 9.3u Sum|x| / c;
+//  * both: + 2^-140 for subnormal intermediates.
+// A group is certified when every decision is constant on the intervals: the
+// zero and the scale are evaluated at both ends (directed rounding; the
+// scale's own float32 roundings covered by 1 -+ 2^-22), and every quotient
+// RN(RN(S sc - z) r) must lie farther than tau = D / s + 2^-21 (|t| + 1)
 // from its rounding boundary.  A certified row's bytes equal the reference's;
-// a row with an uncertified group goes to the float64 pass (k_had64_list, the
-// reference's butterfly in stage order), and rows with non-finite or huge
-// inputs straight to the exact fixup pass (k_encode_fixup).
+// a row with an uncertified group is flagged in a bitmap for the float64 pass
+// (k_had64_list, the reference's butterfly in stage order), and rows with
+// non-finite or huge inputs go straight to the exact fixup pass
+// (k_encode_fixup).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float min3f(float a, float b, float c) {
   float d;
