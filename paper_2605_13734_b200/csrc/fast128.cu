@@ -665,7 +665,7 @@ __host__ __device__ constexpr int enc_tile_bytes() {
 }
 template <bool F32>
 __host__ __device__ constexpr int enc_smem_bytes() {
-  return enc_stages<F32>() * enc_tile_bytes<F32>() + 1024 + 64;
+  return enc_stages<F32>() * enc_tile_bytes<F32>() + 1024 + 128;
 }
 
 // PAGED: bf16 input read from a paged cache (5D boxes per page run); a
@@ -690,12 +690,23 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
   const Geo& g = a.g;
   const int64_t nrows = g.LH * g.T;
   const int64_t ntiles = (nrows + kRows - 1) / kRows;
-  const int tid = threadIdx.x, half = tid & 1;
+  const int tid = threadIdx.x, half = tid & 1, warp = tid >> 5, lane = tid & 31;
+  // certified contiguous bf16 path: every warp streams its own 16-row tiles
+  // through its own 3-slot ring (4 KB boxes, its own mbarriers), so no warp
+  // ever waits for another one (the map's box is 32 half rows)
+  constexpr bool WR = CERT != 0 && !PAGED && !F32;
+  constexpr int WTB = 16 * 256;
+  const int64_t nwt = (nrows + 15) / 16;
 
   // tensor-map coordinate of a tile: 128-byte box rows (bf16 half rows,
   // fp32 quarter rows)
   constexpr int kBoxRows = F32 ? 4 * kRows : 2 * kRows;
-  if (tid == 0) {
+  if constexpr (WR) {
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s) mbar_init(&full[warp * NS + s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  } else if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       slot_arrivals[s] = 0;
@@ -713,7 +724,22 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     else
       tma_load_2d(tiles + s * TB, &tmap, 0, (int)(tile * kBoxRows), &full[s]);
   };
-  if (tid == 0) {
+  auto issue_w = [&](int s, int64_t wt) {  // one warp tile into this warp's slot s
+    uint64_t* b = &full[warp * NS + s];
+    mbar_expect_tx(b, WTB);
+    tma_load_2d(tiles + (warp * NS + s) * WTB, &tmap, 0, (int)(wt * 32), b);
+  };
+  const int64_t t_begin = WR ? (int64_t)blockIdx.x * (kThreads / 32) + warp : (int64_t)blockIdx.x;
+  const int64_t t_end = WR ? nwt : ntiles;
+  const int64_t t_step = WR ? (int64_t)gridDim.x * (kThreads / 32) : (int64_t)gridDim.x;
+  if constexpr (WR) {
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s) {
+        const int64_t wt = t_begin + (int64_t)s * t_step;
+        if (wt < t_end) issue_w(s, wt);
+      }
+    }
+  } else if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < ntiles) issue(s, tile);
@@ -745,13 +771,13 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
     if constexpr (F32) return w[i];
     return (i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16);
   };
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = t_begin; tile < t_end; tile += t_step, ++it) {
     const int s = it % NS;
-    mbar_wait(&full[s], (uint32_t)((it / NS) & 1));
-    const uint8_t* tb = tiles + s * TB;
+    mbar_wait(WR ? &full[warp * NS + s] : &full[s], (uint32_t)((it / NS) & 1));
+    const uint8_t* tb = WR ? tiles + (warp * NS + s) * WTB : tiles + s * TB;
     uint32_t wv[NW];
-    load_half(tb, tid, wv);
-    const int64_t row = tile * kRows + (tid >> 1);
+    load_half(tb, WR ? lane : tid, wv);
+    const int64_t row = WR ? tile * 16 + (lane >> 1) : tile * kRows + (tid >> 1);
     const bool valid = row < nrows;
     // (layer*head, token) of the row: not needed for uniform compile-time
     // widths (the row's stream bit is row * 128 * W) outside delta / affine
@@ -773,7 +799,17 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
         }
       }
     }
-    if constexpr (CERT != 0) {
+    if constexpr (WR) {
+      // this warp's half rows are in registers: refill its slot
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t next = tile + (int64_t)NS * t_step;
+        if (next < t_end) {
+          fence_proxy_async();
+          issue_w(s, next);
+        }
+      }
+    } else if constexpr (CERT != 0) {
       // this warp's half rows are in registers; the warp completing the
       // slot's four arrivals (a monotonic count) refills it
       __syncwarp();
@@ -914,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, ((MODE == M_HADAMARD && !CERT) || MO
         m = (m | (m >> 2)) & 0x0F0F0F0Fu;
         m = (m | (m >> 4)) & 0x00FF00FFu;
         m = (m | (m >> 8)) & 0x0000FFFFu;
-        const int64_t row0 = tile * kRows + (tid & ~31) / 2;
+        const int64_t row0 = WR ? tile * 16 : tile * kRows + (tid & ~31) / 2;
         if ((tid & 31) == 0 && m) atomicOr(a.fix1_bits + (row0 >> 5), m << (row0 & 31));
       }
       if (!row_ok && half == 0 && valid) a.fix_rows[atomicAdd(a.fix_count, 1u)] = (int32_t)row;
@@ -1730,7 +1766,9 @@ cudaError_t launch_encode_fast128(const EncArgs& a, int sm_count, cudaStream_t s
     if (f32 || !paged_input_ok(a) || !make_paged_map(&map, const_cast<void*>(a.kv), a.g, a.layer_stride,
                                                      (int)std::min<int64_t>(a.page_tokens, kRows)))
       return launch_encode_generic(a, s);
-  } else if (!(f32 ? make_input_map_f32(&map, a.kv, nrows) : make_input_map(&map, a.kv, nrows))) {
+  } else if (!(f32 ? make_input_map_f32(&map, a.kv, nrows)
+                   : make_input_map(&map, a.kv, nrows,
+                                    (a.g.transform == T_HADAMARD && a.fix1_bits) ? 32 : kThreads))) {
     return launch_encode_generic(a, s);
   }
   cudaError_t e;
